@@ -1,0 +1,237 @@
+"""Pins for O2 (schedule), O3 (layer) and O4 (simulated EP / LLEP) -- CPU only."""
+import json
+import math
+import os
+import random
+
+import numpy as np
+import pytest
+
+from oracle import layer as O3
+from oracle import planner as O1
+from oracle import schedule as O2
+from oracle import simulate as O4
+from synth import workload as W
+
+
+def _load(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as f:
+        return json.load(f)
+
+
+# ------------------------------------------------------------------ O2
+def test_reindex_worked_examples(golden_dir):
+    g = _load(golden_dir, "schedule_examples.json")
+    ex = g["reindex"][0]
+    ids = np.array(ex["ids"])
+    perm, sorted_ids = O2.stable_reindex(ids)
+    assert perm.tolist() == ex["sorted_tokens"]
+    cnt = O2.local_counts(ids, ex["n_experts"])
+    assert {str(e): int(c) for e, c in enumerate(cnt) if c} == ex["counts"]
+    ex = g["reindex"][1]
+    ids = np.array(ex["ids"])
+    perm, sorted_ids = O2.stable_reindex(ids)
+    assert perm[sorted_ids == 0].tolist() == ex["expert0_flat_slots"]
+    r = O2.local_rank_in_expert(ids)
+    assert r.tolist() == [0, 0, 1, 1, 2, 2]
+
+
+def test_materialize_example(golden_dir):
+    ex = _load(golden_dir, "schedule_examples.json")["materialize"][0]
+    C = np.array(ex["C"])
+    plan = O1.Plan(2, 2, [[tuple(c) for c in A] for A in ex["chunks"]], [5, 5], 5, 10, False)
+    sch = O2.send_schedule(plan, C)
+    for key, sl in ex["slices"].items():
+        p, e = map(int, key.split(","))
+        assert [list(s) for s in sch[(p, e)]] == sl
+
+
+def test_out_of_range_ids():
+    with pytest.raises(ValueError):
+        O2.local_counts(np.array([[0, 5]]), 4)
+
+
+def _check_destinations(plan, C, ids_per_rank):
+    """Every (token, slot) pair lands exactly once; per (e, d) positions are 0..rows-1."""
+    seen = {}
+    for p, ids in enumerate(ids_per_rank):
+        dev, pos = O2.slot_destinations(plan, C, ids, p)
+        flat = ids.reshape(-1)
+        for j in range(flat.size):
+            key = (int(flat[j]), int(dev[j]))
+            seen.setdefault(key, []).append(int(pos[j]))
+    for e in range(plan.n_experts):
+        for d in range(plan.world):
+            n = O2.rows_on_device(plan, e, d)
+            got = sorted(seen.get((e, d), []))
+            assert got == list(range(n)), (e, d)
+
+
+def test_destinations_fuzz():
+    rng = np.random.default_rng(7)
+    for trial in range(60):
+        P = int(rng.choice([1, 2, 3, 4]))
+        M = int(rng.integers(1, 4))
+        N = P * M
+        K = int(rng.integers(1, 4))
+        B = int(rng.integers(0, 40))
+        hot = int(rng.integers(0, N))
+        ids = []
+        for p in range(P):
+            x = rng.integers(0, N, size=(B, K))
+            x[rng.random((B, K)) < 0.6] = hot
+            ids.append(x.astype(np.int32))
+        C = O2.load_matrix(ids, N)
+        plan = O1.plan(C.sum(0).tolist(), P, 1.0, int(rng.choice([0, 1, 3, 50])), 1.0)
+        _check_destinations(plan, C, ids)
+        # schedule consistency: destination totals per (e, d) == chunk sizes
+        sch = O2.send_schedule(plan, C)
+        for e in range(N):
+            for d in range(P):
+                tot = sum(b - a for p in range(P) for (dd, a, b) in sch[(p, e)] if dd == d)
+                assert tot == O2.rows_on_device(plan, e, d)
+
+
+# ------------------------------------------------------------------ O3
+def test_linear_hand_value():
+    """D=2, N=2, K=1, u=[1,0], gate 0.8808, W_0 = [[1],[1]] (H=1) -> h = 0.8808."""
+    x = np.array([[1.0, 0.0]])
+    ids = np.array([[0]])
+    g = np.array([[0.8808]])
+    Ws = {0: np.array([[1.0], [1.0]]), 1: np.array([[5.0], [7.0]])}
+    h = O3.moe_forward_linear(x, ids, g, lambda e: Ws[e])
+    assert h.shape == (1, 1) and h[0, 0] == pytest.approx(0.8808, abs=1e-15)
+
+
+def test_swiglu_hand_values():
+    """1-D SwiGLU: u=2, w_gate=ln3/2 -> z=ln 3, silu(ln 3) = ln3 · 3/4 (sigmoid(ln 3) = 3/4);
+    w_up=5 -> 10; w_down=0.5 -> FFN = 0.5 · 0.75 ln3 · 10 = 3.75 ln 3.  Swapping gate/up, a sign
+    error in the sigmoid or dropping W_down all change the value."""
+    w = (np.array([[math.log(3) / 2]]), np.array([[5.0]]), np.array([[0.5]]))
+    y = O3.swiglu_ffn(np.array([[2.0]]), w)
+    assert y[0, 0] == pytest.approx(3.75 * math.log(3), rel=1e-14)
+    # 2-D case: orientation of W_gate [H, D], W_up [H, D], W_down [D, H] (D=2, H=1)
+    wg = np.array([[math.log(3), 0.0]])       # z = ln3 · u0
+    wu = np.array([[0.0, 2.0]])               # up = 2 · u1
+    wd = np.array([[1.0], [-3.0]])            # out = [a, -3a]
+    y = O3.swiglu_ffn(np.array([[1.0, 4.0]]), (wg, wu, wd))
+    a = 0.75 * math.log(3) * 8.0
+    assert y[0].tolist() == pytest.approx([a, -3 * a], rel=1e-14)
+
+
+def _rand_weights(rng, D, H):
+    return (rng.standard_normal((H, D)) / np.sqrt(D), rng.standard_normal((H, D)) / np.sqrt(D),
+            rng.standard_normal((D, H)) / np.sqrt(H))
+
+
+def test_layer_special_cases():
+    rng = np.random.default_rng(3)
+    D, H, N = 8, 6, 4
+    Ws = {e: _rand_weights(rng, D, H) for e in range(N)}
+    # zero token -> 0
+    out = O3.moe_forward(np.zeros((2, D)), np.array([[0, 1], [2, 3]]), np.ones((2, 2)), Ws.get)
+    assert np.all(out == 0)
+    # gate 0 -> no contribution; all K slots on one expert with gates summing to 1 -> one FFN
+    x = rng.standard_normal((3, D))
+    out = O3.moe_forward(x, np.array([[1, 1, 1]] * 3), np.array([[0.25, 0.5, 0.25]] * 3), Ws.get)
+    ref = O3.swiglu_ffn(x, Ws[1])
+    np.testing.assert_allclose(out, ref, rtol=1e-14, atol=1e-15)
+    out2 = O3.moe_forward(x, np.array([[1, 2, 1]] * 3), np.array([[0.5, 0.0, 0.5]] * 3), Ws.get)
+    np.testing.assert_allclose(out2, ref, rtol=1e-14, atol=1e-15)
+
+
+def test_layer_linearity_in_gates():
+    """Eq. 1 is linear in the gates: out(g1 + g2) = out(g1) + out(g2)."""
+    rng = np.random.default_rng(4)
+    D, H, N, T, K = 16, 8, 5, 12, 3
+    Ws = {e: _rand_weights(rng, D, H) for e in range(N)}
+    x = rng.standard_normal((T, D))
+    ids = rng.integers(0, N, (T, K))
+    g1, g2 = rng.random((T, K)), rng.random((T, K))
+    a = O3.moe_forward(x, ids, g1 + g2, Ws.get)
+    b = O3.moe_forward(x, ids, g1, Ws.get) + O3.moe_forward(x, ids, g2, Ws.get)
+    np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-12)
+
+
+# ------------------------------------------------------------------ O4
+def _sim_case(rng, P, M, K, B, D, H, hot_share, m, lam):
+    N = P * M
+    Ws = {e: _rand_weights(rng, D, H) for e in range(N)}
+    xs, ids, gs = [], [], []
+    for p in range(P):
+        xs.append(rng.standard_normal((B, D)))
+        i = rng.integers(0, N, (B, K))
+        i[rng.random((B, K)) < hot_share] = 0
+        ids.append(i)
+        gs.append(rng.random((B, K)))
+    return N, Ws, xs, ids, gs
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_ep_llep_dense_equal(seed):
+    """Exactness: LLEP == EP == dense Eq. 1 within 1e-12 relative, incl. duplicate ids,
+    zero-load experts, force-assign plans and the λ fallback."""
+    rng = np.random.default_rng(100 + seed)
+    P = [1, 2, 3, 4][seed % 4]
+    M = 1 + seed % 3
+    K = 1 + seed % 3
+    B = 5 + 3 * seed
+    N, Ws, xs, ids, gs = _sim_case(rng, P, M, K, B, 6, 5, [0.0, 0.5, 0.9][seed % 3], [0, 2, 7][seed % 3],
+                                   [1.0, 1.3][seed % 2])
+    dense = [O3.moe_forward(xs[p], ids[p], gs[p], Ws.get) for p in range(P)]
+    ep, _, _ = O4.dispatch_combine(xs, ids, gs, Ws.get, N, P, mode="ep")
+    ll, plan, _ = O4.dispatch_combine(xs, ids, gs, Ws.get, N, P, mode="llep",
+                                      min_chunk=[0, 2, 7][seed % 3], lam=[1.0, 1.3][seed % 2])
+    scale = max(np.abs(d).max() for d in dense)
+    for p in range(P):
+        assert np.abs(ep[p] - dense[p]).max() <= 1e-12 * scale
+        assert np.abs(ll[p] - dense[p]).max() <= 1e-12 * scale
+
+
+def test_llep_spills_and_forces_are_exercised():
+    rng = np.random.default_rng(9)
+    seen_force = seen_transfer = False
+    for t in range(30):
+        N, Ws, xs, ids, gs = _sim_case(rng, 3, 2, 2, 15, 4, 3, 0.6, 20, 1.0)
+        dense = [O3.moe_forward(xs[p], ids[p], gs[p], Ws.get) for p in range(3)]
+        ll, plan, st = O4.dispatch_combine(xs, ids, gs, Ws.get, N, 3, mode="llep", min_chunk=20, lam=1.0)
+        seen_force |= plan.force_count > 0
+        seen_transfer |= len(plan.transfers) > 0
+        for p in range(3):
+            np.testing.assert_allclose(ll[p], dense[p], rtol=1e-12, atol=1e-12)
+    assert seen_force and seen_transfer
+
+
+def test_workload_shapes_and_slot_fractions():
+    """The synthetic scenario: hot ids 0..y-1 get x/y of all slots each."""
+    sh = W.CONFIGS["g120"]
+    for pct, y in [(95, 1), (50, 4), (30, 16)]:
+        c = W.slot_counts(sh.n_experts, sh.tokens_per_rank * sh.top_k, pct, y)
+        assert c.sum() == sh.tokens_per_rank * sh.top_k
+        hot = c[:y].sum() / c.sum()
+        assert abs(hot - pct / 100) < 1e-4
+        assert c[:y].max() - c[:y].min() <= 1 and c[y:].max() - c[y:].min() <= 1
+    ids = W.routing_ids(W.CONFIGS["tiny"], 0, 95, 1)
+    assert ids.shape == (1024, 2) and ids.dtype == np.int32
+    assert np.bincount(ids.ravel(), minlength=8).tolist() == W.slot_counts(8, 2048, 95, 1).tolist()
+    g = W.gate_weights(16, 4, 0)
+    assert np.all(g > 0) and np.allclose(g.sum(1), 1.0, atol=1e-6)
+
+
+def test_generator_numpy_torch_identical():
+    """The counter-based generator gives identical bf16 bits on numpy and torch (CPU here)."""
+    import torch
+    bits = W.tokens_bits(7, 33, 3)
+    t = W.tokens_torch(7, 33, 3, "cpu")
+    assert np.array_equal(t.view(torch.int16).numpy().view(np.uint16), bits)
+    rows = W.token_rows_bits(np.array([5, 0, 2]), 33, 3)
+    assert np.array_equal(rows, bits[[5, 0, 2]])
+    wg, wu, wd = W.expert_weights_bits(5, 24, 16)
+    w13, w2 = W.expert_weights_torch([5], 24, 16, "cpu")
+    assert np.array_equal(w13[0, :16].view(torch.int16).numpy().view(np.uint16), wg)
+    assert np.array_equal(w13[0, 16:].view(torch.int16).numpy().view(np.uint16), wu)
+    assert np.array_equal(w2[0].view(torch.int16).numpy().view(np.uint16), wd)
+    # bf16 RNE rounding matches torch's conversion on awkward values
+    f = np.array([1.0, 1.00390625, 1.01171875, -3.0e-39, 65504.0, 1e30], dtype=np.float32)
+    assert np.array_equal(W.bf16_bits_from_f32(f),
+                          torch.from_numpy(f).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16))

@@ -1,0 +1,229 @@
+/*
+ * llep.h -- C ABI of the B200-native Least-Loaded Expert Parallelism (LLEP) hot path.
+ *
+ * Paper: "Least-Loaded Expert Parallelism", arxiv 2601.17111 (text in PAPER.md; P:n = line n).
+ * The problem as the paper states it: per device p, tokens B_p, router weights G_p and indices
+ * I_p, and the local expert weights W_i, i in [pM, (p+1)M) -> the MoE output H'_p
+ * (Alg. 4 header/output).  The planner takes the global loads l, M (hence P), α, m
+ * (Alg. 2 input) and λ (Alg. 4).
+ *
+ * Conventions
+ *   - Every pointer is plain host or device memory as stated per argument; no framework types.
+ *   - Tensors are caller-owned.  The library never frees a caller pointer and keeps none past
+ *     the call, except the context's OWN symmetric arena (see llep_context_*).
+ *   - Device calls are stream-ordered on the caller's `stream` (a cudaStream_t passed as void*).
+ *   - Return codes only; no exception crosses the ABI.  llep_last_error() gives a message
+ *     (thread-local) naming the first violated condition.
+ *   - Layouts are row-major.  bf16 = IEEE bfloat16 bit patterns (uint16_t).
+ *   - Shapes: N experts, K = top-k, D = d_model, H = d_ff, P = EP world size, M = N / P,
+ *     B = tokens on this rank.  Expert e is native to device floor(e / M) (Alg. 2).
+ */
+#ifndef LLEP_H
+#define LLEP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status codes */
+typedef enum {
+  LLEP_OK = 0,
+  LLEP_ERR_INVALID = 1,  /* bad argument: N % P != 0, K not in [1,N], D/H/P < 1, α < 1, λ < 1,
+                            m < 0, negative load, misaligned / null pointer, unsupported shape  */
+  LLEP_ERR_PLAN = 2,     /* plan inconsistent with the loads (chunk totals != l_e), or too
+                            large for the context's arena (call llep_context_reserve first)     */
+  LLEP_ERR_ROUTING = 3,  /* a router index outside [0, N) (detected on device, reported by the
+                            next call that synchronises: llep_prepare)                          */
+  LLEP_ERR_NOMEM = 4,    /* device allocation failed                                           */
+  LLEP_ERR_CUDA = 5,     /* CUDA runtime / driver error                                        */
+  LLEP_ERR_COMM = 6      /* peer mapping or device-barrier failure (timeout)                    */
+} llep_status;
+
+const char *llep_last_error(void);
+const char *llep_version(void);
+
+/* ------------------------------------------------------------------ parameters */
+/* Planner constraints (§4 "Constraints"): α >= 1 scales the per-device capacity
+ * m_α = α·Σl/P; m >= 0 is the minimum tokens per spilled GEMM chunk; λ >= 1 is the imbalance
+ * threshold below which standard EP runs (max(l)/mean(l) < λ, Alg. 4).  The paper's
+ * settings are α=1, m=1024, λ=1.3. */
+typedef struct {
+  double alpha;
+  int64_t min_chunk;
+  double lambda;
+} llep_params;
+
+/* ------------------------------------------------------------------ plan blob
+ * A plan is one contiguous, caller-owned buffer of llep_plan_bytes(N, P) bytes, identical in
+ * host and device memory, laid out as:
+ *
+ *   offset 0                 llep_plan_header
+ *   hdr.off_assigned         int64_t    assigned[P]        g_a: rows device d computes
+ *   hdr.off_n_chunks         int32_t    n_chunks[N]        chunks of expert e (0 if l_e == 0)
+ *   hdr.off_chunks           llep_chunk chunks[N][P+1]     𝒜[e] in plan order; unused slots 0
+ *   hdr.off_replica          uint8_t    replica[N][P]      𝒲: 1 iff e has a chunk on d != native
+ *
+ * 𝒜 (Alg. 2 output): expert e's global token range [0, l_e) is split into chunks
+ * (device, start, end), in the order LLA/LLAS appended them; the native chunk (Case 1/2) first.
+ * An expert can hold two chunks on one device (accepted spill + force-assign), and never more
+ * than P+1 chunks (each non-final LLAS chunk fills a distinct device to capacity).
+ * 𝒲: transfer of W_e from native(e) to every d with replica[e][d] = 1.
+ * Two plans for the same inputs are bit-identical (host and device planners included). */
+typedef struct {
+  int32_t device, start, end;
+} llep_chunk;
+
+typedef struct {
+  int32_t n_experts, world_size, max_chunks; /* max_chunks = P + 1                          */
+  int32_t fallback_ep;   /* 1 iff S == 0 or max(l)/(S/N) < λ -> all-native plan  */
+  int32_t force_count;   /* LLAS force-assigns; if > 0 a device may exceed cap   */
+  int32_t n_transfers;   /* |𝒲|                                                             */
+  int64_t total;         /* S = Σ l                                                          */
+  int64_t capacity;      /* cap = floor((α·S)/P) in IEEE double, no FMA (m_α)         */
+  int64_t max_assigned;  /* max_d g_a[d]                                                     */
+  int32_t off_assigned, off_n_chunks, off_chunks, off_replica;
+} llep_plan_header;
+
+size_t llep_plan_bytes(int32_t n_experts, int32_t world_size);
+
+/* llep_plan -- the LLEP planner on the host (Alg. 4 head P:537-541, Alg. 2 P:382-423,
+ * Alg. 3, 𝒲 P:420).
+ *   loads     [N] int64, host: global per-expert loads l (slot counts summed over ranks)
+ *   plan_out  host buffer of llep_plan_bytes(N, P) bytes (written completely)
+ * Readings of the paper's silent points are listed in DESIGN.md §Readings (R1-R9): integer
+ * capacity, no empty chunks, skip of c <= 0 candidates, ties by (load desc, id asc) and
+ * (g_a+g_p asc, id asc), whole-remainder force-assign.
+ * Errors: LLEP_ERR_INVALID (N % P, α < 1, λ < 1, m < 0, negative load, null). Pure, re-entrant. */
+llep_status llep_plan(const int64_t *loads, int32_t n_experts, int32_t world_size,
+                      const llep_params *params, void *plan_out);
+
+/* llep_plan_ep -- the all-native plan of standard EP (Alg. 1) on the host;
+ * fallback_ep = 0 (it is the baseline, not the λ fallback). */
+llep_status llep_plan_ep(const int64_t *loads, int32_t n_experts, int32_t world_size,
+                         const llep_params *params, void *plan_out);
+
+/* llep_plan_device -- the same planner as a one-warp device kernel (bit-identical blob).
+ *   load_matrix  [P, N] int32, device: C[q][e] = rank q's slots routed to e; l = column sums
+ *   plan_out     device buffer of llep_plan_bytes(N, P) bytes
+ *   force_ep     0: LLEP (λ test + LLA); 1: standard-EP plan
+ * Requires P <= 32.  Errors: LLEP_ERR_INVALID, LLEP_ERR_CUDA. */
+llep_status llep_plan_device(const int32_t *load_matrix, int32_t n_experts, int32_t world_size,
+                             const llep_params *params, int32_t force_ep, void *plan_out,
+                             void *stream);
+
+/* ------------------------------------------------------------------ context (one per rank)
+ * The context owns this rank's symmetric arena: load-matrix slots, barrier flags, receive rows
+ * X [R, D] bf16 + gates [R] fp32, expert-FFN outputs Y [R, D] bf16, activations A [R, H] bf16
+ * and imported (foreign) expert weights.  Peers map each other's arenas through CUDA IPC so
+ * the dispatch stores and combine loads go straight over NVLink (no staging copies). */
+typedef struct llep_context llep_context;
+
+typedef struct {
+  int32_t n_experts, top_k, d_model, d_ff, world_size;
+} llep_shape;
+
+/* Create the context for `rank` on CUDA device `device` (the caller's current device).
+ * max_tokens: largest B this rank will pass.  Allocates the rank-local scratch and an initial
+ * arena (grown by llep_context_reserve).  Errors: INVALID (shape rules above; D, H % 8 != 0;
+ * P > 32), NOMEM, CUDA. */
+llep_status llep_context_create(const llep_shape *shape, int32_t rank, int32_t device,
+                                int64_t max_tokens, llep_context **out);
+void llep_context_destroy(llep_context *ctx);
+
+/* Symmetric-arena bootstrap.  Every rank calls get_handle, the caller all-gathers the P
+ * 64-byte handles (any transport; the library needs only the bytes), and every rank calls
+ * open_peers with the gathered [P][64] array.  P == 1 needs neither call. */
+llep_status llep_context_ipc_handle(llep_context *ctx, void *handle64);
+llep_status llep_context_open_peers(llep_context *ctx, const void *handles, int32_t n);
+
+/* Grow the arena so every rank can receive `rows` padded rows and `foreign` imported experts.
+ * Collective: all ranks must call it with the same arguments, then redo the handle exchange.
+ * The numbers come from llep_requirements (identical on every rank). */
+llep_status llep_context_reserve(llep_context *ctx, int64_t rows, int32_t foreign);
+
+/* Bytes the context currently holds on the device (arena + scratch). */
+int64_t llep_context_device_bytes(const llep_context *ctx);
+
+/* Needs of one plan, identical on every rank (the plan is replicated and deterministic). */
+typedef struct {
+  int64_t rows_needed;     /* max_d padded receive rows of device d (groups 128-row aligned)  */
+  int32_t foreign_needed;  /* max_d |S_d|                                                      */
+  int32_t fits;            /* 1 iff both fit this context's current arena                      */
+  int64_t my_rows;         /* g_a[rank]                                                         */
+  int32_t my_groups;       /* expert groups this rank computes (native with rows + foreign)    */
+  int32_t fallback_ep, force_count, n_transfers;
+} llep_requirements;
+
+/* ------------------------------------------------------------------ the hot path
+ * llep_prepare -- steps 1-2 of the path for this rank (Alg. 4):
+ *   a1  local load histogram of topk_ids (per-tile counts, stable per-expert local ranks)
+ *   a2  exchange: push this rank's counts row to every peer, device barrier -> C [P, N]
+ *   a4  planner kernel on C (λ test, LLA, LLAS, 𝒲) -> plan_out (device blob)
+ *   a5  layout: per-device expert groups (native first, then foreign), 128-row aligned bases
+ * then one device->host read of the requirements (needed to size the arena; the only host
+ * synchronisation of the layer).
+ *   topk_ids   [B, K] int32, device.  Ids outside [0, N) -> LLEP_ERR_ROUTING.
+ *   force_ep   1 -> standard EP plan on the same kernels (Alg. 1); 0 -> LLEP.
+ *   plan_out   device buffer, llep_plan_bytes(N, P).
+ *   req        host, may be NULL.
+ * All ranks must call llep_prepare and llep_moe_forward the same number of times (barriers). */
+llep_status llep_prepare(llep_context *ctx, const int32_t *topk_ids, int64_t n_tokens,
+                         const llep_params *params, int32_t force_ep, void *plan_out,
+                         llep_requirements *req, void *stream);
+
+/* llep_moe_forward -- steps 3-4 (Alg. 4) with the plan from llep_prepare:
+ *   a6  dispatch: gather-on-send of x rows + gates straight from the unsorted inputs into the
+ *       destination device's receive rows (NVLink peer stores; local rows stay in HBM)
+ *   a7  weight migration: copy-engine push of W13_e, W2_e native(e) -> d for every 𝒲 entry
+ *   a8  grouped GEMM1 + SwiGLU: A = silu(X W_gateᵀ) ⊙ (X W_upᵀ)   (tcgen05/TMEM/TMA)
+ *   a9  grouped GEMM2 + gate:   Y = diag(g) · (A W_downᵀ)          (Ĥ = Ĝ ⊙ B̂W)
+ *   a10 combine: out[t] = Σ_{k=0..K-1} Y[dst(t,k)] in slot order, fp32, one bf16 rounding
+ *       (reverse All-to-All + reverse sort + sum over K), pulled over NVLink.
+ *   x          [B, D] bf16, device      topk_ids [B, K] int32     topk_w [B, K] fp32
+ *   w13        [M, 2H, D] bf16: rows 0..H-1 = W_gate,e, rows H..2H-1 = W_up,e (native experts)
+ *   w2         [M, D, H] bf16 = W_down,e
+ *   plan       device blob from llep_prepare of these topk_ids
+ *   out        [B, D] bf16, device
+ * Errors: INVALID, PLAN (plan larger than the arena), CUDA, COMM. */
+llep_status llep_moe_forward(llep_context *ctx, const uint16_t *x, const int32_t *topk_ids,
+                             const float *topk_w, int64_t n_tokens, const uint16_t *w13,
+                             const uint16_t *w2, const void *plan, uint16_t *out, void *stream);
+
+/* ------------------------------------------------------------------ inspection (tests)
+ * Copy the last prepare/forward intermediates to caller DEVICE buffers (sizes in elements):
+ *   LLEP_DBG_LOAD_MATRIX  int32 [P*N]        LLEP_DBG_SLOT_DST  int32 [2*B*K] (device,row)
+ *   LLEP_DBG_GROUPS       int32 [G*8]        (expert, weight slot (-1-f = foreign f), row_base,
+ *                                             n_rows, mblk_start, 0, 0, 0), G = my_groups
+ *   LLEP_DBG_RECV_X       bf16 [rows*D]      LLEP_DBG_ACT bf16 [rows*H]   LLEP_DBG_Y bf16 [rows*D]
+ *   LLEP_DBG_LOCAL_RANK   int32 [B*K]  (r_j: rank of slot j among this rank's slots of ids[j]) */
+enum {
+  LLEP_DBG_LOAD_MATRIX = 1,
+  LLEP_DBG_SLOT_DST = 2,
+  LLEP_DBG_GROUPS = 3,
+  LLEP_DBG_RECV_X = 4,
+  LLEP_DBG_ACT = 5,
+  LLEP_DBG_Y = 6,
+  LLEP_DBG_LOCAL_RANK = 7,
+  LLEP_DBG_RECV_G = 8
+};
+llep_status llep_debug_copy(llep_context *ctx, int32_t what, void *dst, int64_t n_elems,
+                            void *stream);
+
+/* Standalone grouped-GEMM entry (kernel tests / micro-bench, the paper's F-gemm shape P:1127):
+ * rows of group g occupy [row_base[g], row_base[g]+n_rows[g]) of a, with row_base % 128 == 0.
+ *   mode 0: out[r, 0:Hn] = silu(a W[e][0:Hn]ᵀ) ⊙ (a W[e][Hn:2Hn]ᵀ),  W [E, 2Hn, Kd], out [R, Hn]
+ *   mode 1: out[r, 0:Nn] = gate[r] · (a W[e]ᵀ),                      W [E, Nn, Kd],  out [R, Nn]
+ * groups: HOST int32 [G*4] = (expert, row_base, n_rows, 0), increasing non-overlapping rows.
+ * Errors: INVALID (mode, ranges, alignment), CUDA. */
+llep_status llep_grouped_gemm(int32_t mode, const uint16_t *a, int64_t rows, int32_t kdim,
+                              const uint16_t *w, int32_t n_weights, int32_t nout,
+                              const int32_t *groups, int32_t n_groups, const float *gate,
+                              uint16_t *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LLEP_H */

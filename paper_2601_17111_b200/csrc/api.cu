@@ -1,0 +1,748 @@
+// C ABI of the LLEP hot path (include/llep.h): host planner, per-rank context with a CUDA-IPC
+// symmetric arena, and the two stream-ordered calls llep_prepare / llep_moe_forward.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace llep {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+llep_status cuda_status(cudaError_t e, const char *what) {
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? LLEP_ERR_NOMEM : LLEP_ERR_CUDA;
+}
+
+static llep_status invalid(const char *msg) {
+  set_error("%s", msg);
+  return LLEP_ERR_INVALID;
+}
+
+static llep_status check_params(const llep_params *p) {
+  if (!p) return invalid("params is null");
+  if (!(p->alpha >= 1.0)) return invalid("alpha < 1");
+  if (!(p->lambda >= 1.0)) return invalid("lambda < 1");
+  if (p->min_chunk < 0) return invalid("min_chunk < 0");
+  return LLEP_OK;
+}
+
+static llep_status check_np(int32_t N, int32_t P) {
+  if (P < 1 || N < 1) return invalid("N and P must be >= 1");
+  if (N % P != 0) return invalid("N not divisible by P");
+  if (N > kMaxGroups) return invalid("N > 1024 experts is not supported");
+  return LLEP_OK;
+}
+
+// ------------------------------------------------------------------ host planner
+// Sequential twin of planner_kernel (plan.cu); same decisions, same IEEE double operations.
+static void host_plan(const int64_t *l, int32_t N, int32_t P, const llep_params *prm,
+                      bool force_ep, uint8_t *blob) {
+  const PlanLayout L = plan_layout(N, P);
+  memset(blob, 0, L.bytes);
+  llep_plan_header *hdr = reinterpret_cast<llep_plan_header *>(blob);
+  int64_t *assigned = reinterpret_cast<int64_t *>(blob + L.off_assigned);
+  int32_t *n_chunks = reinterpret_cast<int32_t *>(blob + L.off_n_chunks);
+  llep_chunk *chunks = reinterpret_cast<llep_chunk *>(blob + L.off_chunks);
+  uint8_t *replica = blob + L.off_replica;
+  const int MC = P + 1, M = N / P;
+  int64_t S = 0, maxl = 0;
+  for (int e = 0; e < N; ++e) {
+    S += l[e];
+    maxl = std::max(maxl, l[e]);
+  }
+  volatile double prod = prm->alpha * (double)S;  // volatile: one rounding per operation
+  volatile double mal = prod / (double)P;
+  const int64_t cap = (int64_t)std::floor((double)mal);
+  bool fallback = (S == 0);
+  if (!fallback) {
+    volatile double mean = (double)S / (double)N;
+    volatile double ratio = (double)maxl / (double)mean;
+    fallback = ratio < prm->lambda;
+  }
+  int forces = 0;
+  std::vector<int64_t> ga(P, 0), gp(P, 0);
+  if (force_ep || fallback) {
+    for (int e = 0; e < N; ++e)
+      if (l[e] > 0) {
+        chunks[(size_t)e * MC] = llep_chunk{e / M, 0, (int32_t)l[e]};
+        n_chunks[e] = 1;
+        ga[e / M] += l[e];
+      }
+  } else {
+    std::vector<int> order(N);
+    for (int e = 0; e < N; ++e) order[e] = e;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return l[a] > l[b]; });
+    for (int e = 0; e < N; ++e) gp[e / M] += l[e];
+    for (int idx = 0; idx < N; ++idx) {
+      const int e = order[idx];
+      const int64_t le = l[e];
+      if (le == 0) break;
+      const int ng = e / M;
+      gp[ng] -= le;
+      const int64_t na = cap - ga[ng] - gp[ng];
+      llep_chunk *A = chunks + (size_t)e * MC;
+      int nc = 0;
+      int64_t r, to;
+      if (na >= le) {
+        A[nc++] = llep_chunk{ng, 0, (int32_t)le};
+        ga[ng] += le;
+        r = 0;
+        to = le;
+      } else if (na > 0) {
+        A[nc++] = llep_chunk{ng, 0, (int32_t)na};
+        ga[ng] += na;
+        r = le - na;
+        to = na;
+      } else {
+        r = le;
+        to = 0;
+      }
+      while (r > 0) {
+        int sel = -1, force_sel = -1;
+        int64_t csel = 0, best = 0, fbest = 0;
+        for (int o = 0; o < P; ++o) {
+          if (o == ng) continue;
+          const int64_t load = ga[o] + gp[o];
+          if (force_sel < 0 || load < fbest) {
+            force_sel = o;
+            fbest = load;
+          }
+          const int64_t c = std::min(r, cap - load);
+          if (c <= 0 || (c < prm->min_chunk && r > c)) continue;
+          if (sel < 0 || load < best) {
+            sel = o;
+            best = load;
+            csel = c;
+          }
+        }
+        if (sel < 0) {
+          sel = force_sel;
+          csel = r;
+          ++forces;
+        }
+        A[nc++] = llep_chunk{sel, (int32_t)to, (int32_t)(to + csel)};
+        ga[sel] += csel;
+        r -= csel;
+        to += csel;
+      }
+      n_chunks[e] = nc;
+    }
+  }
+  int ntr = 0;
+  for (int e = 0; e < N; ++e)
+    for (int c = 0; c < n_chunks[e]; ++c) {
+      const int d = chunks[(size_t)e * MC + c].device;
+      if (d != e / M && !replica[(size_t)e * P + d]) {
+        replica[(size_t)e * P + d] = 1;
+        ++ntr;
+      }
+    }
+  int64_t mx = 0;
+  for (int d = 0; d < P; ++d) {
+    assigned[d] = ga[d];
+    mx = std::max(mx, ga[d]);
+  }
+  hdr->n_experts = N;
+  hdr->world_size = P;
+  hdr->max_chunks = MC;
+  hdr->fallback_ep = (!force_ep && fallback) ? 1 : 0;
+  hdr->force_count = (force_ep || fallback) ? 0 : forces;
+  hdr->n_transfers = ntr;
+  hdr->total = S;
+  hdr->capacity = cap;
+  hdr->max_assigned = mx;
+  hdr->off_assigned = L.off_assigned;
+  hdr->off_n_chunks = L.off_n_chunks;
+  hdr->off_chunks = L.off_chunks;
+  hdr->off_replica = L.off_replica;
+}
+
+}  // namespace llep
+
+using namespace llep;
+
+// ====================================================================== context
+struct llep_context {
+  int32_t N, K, D, H, P, M, rank, device, num_sms;
+  int64_t max_tokens;
+  // rank-local scratch
+  int32_t *tile_cnt = nullptr, *tile_off = nullptr, *cnt = nullptr, *local_rank = nullptr;
+  int32_t *slot_dst = nullptr, *err = nullptr, *lm_local = nullptr;
+  int32_t *rows_on = nullptr, *chunk_row = nullptr, *foreign_slot = nullptr;
+  int32_t *dev_padded = nullptr, *dev_foreign = nullptr;
+  Group *groups = nullptr;
+  LayoutSummary *summary = nullptr;
+  LayoutSummary *summary_host = nullptr;  // pinned
+  int32_t *err_host = nullptr;            // pinned
+  uint16_t *act = nullptr;                // A [arena_rows, H]
+  size_t scratch_bytes = 0;
+  // symmetric arena
+  uint8_t *arena = nullptr;
+  size_t arena_bytes = 0;
+  int64_t arena_rows = 0;
+  int32_t arena_foreign = 0;
+  size_t off_flags = 0, off_lm = 0, off_x = 0, off_g = 0, off_w13 = 0, off_w2 = 0;
+  uint8_t *peer_base[kMaxWorld] = {};
+  bool peer_opened[kMaxWorld] = {};
+  bool peers_ready = false;
+  void **d_ptrs = nullptr;  // device: flags[P], lm[P], x[P], g[P]
+  uint32_t epoch = 0;
+  // host copy of the last prepared plan
+  std::vector<uint8_t> plan_host;
+  const void *plan_dev_cached = nullptr;
+  int64_t prepared_tokens = -1;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+};
+
+static void layout_offsets(llep_context *c, int64_t rows, int32_t foreign) {
+  size_t off = 0;
+  c->off_flags = off;
+  off += 256;
+  c->off_lm = off;
+  off = align8(off + sizeof(int32_t) * (size_t)c->P * c->N);
+  off = (off + 1023) & ~size_t(1023);
+  c->off_x = off;
+  off += (size_t)rows * c->D * 2;
+  off = (off + 1023) & ~size_t(1023);
+  c->off_g = off;
+  off += (size_t)rows * 4;
+  off = (off + 1023) & ~size_t(1023);
+  c->off_w13 = off;
+  off += (size_t)foreign * 2 * c->H * c->D * 2;
+  off = (off + 1023) & ~size_t(1023);
+  c->off_w2 = off;
+  off += (size_t)foreign * c->D * c->H * 2;
+  c->arena_bytes = (off + 4095) & ~size_t(4095);
+}
+
+static void close_peers(llep_context *c) {
+  for (int q = 0; q < c->P; ++q) {
+    if (c->peer_opened[q] && c->peer_base[q]) cudaIpcCloseMemHandle(c->peer_base[q]);
+    c->peer_opened[q] = false;
+    c->peer_base[q] = nullptr;
+  }
+  c->peers_ready = false;
+}
+
+static llep_status upload_peer_ptrs(llep_context *c) {
+  std::vector<void *> h(4 * c->P);
+  for (int q = 0; q < c->P; ++q) {
+    uint8_t *b = c->peer_base[q];
+    h[q] = b + c->off_flags;
+    h[c->P + q] = b + c->off_lm;
+    h[2 * c->P + q] = b + c->off_x;
+    h[3 * c->P + q] = b + c->off_g;
+  }
+  LLEP_CUDA(cudaMemcpy(c->d_ptrs, h.data(), sizeof(void *) * 4 * c->P, cudaMemcpyHostToDevice));
+  return LLEP_OK;
+}
+
+static llep_status alloc_arena(llep_context *c, int64_t rows, int32_t foreign) {
+  rows = std::max<int64_t>(rows, kRowAlign);
+  foreign = std::max(foreign, 1);
+  close_peers(c);
+  if (c->arena) cudaFree(c->arena);
+  if (c->act) cudaFree(c->act);
+  c->arena = nullptr;
+  c->act = nullptr;
+  layout_offsets(c, rows, foreign);
+  LLEP_CUDA(cudaMalloc(&c->arena, c->arena_bytes));
+  LLEP_CUDA(cudaMemset(c->arena, 0, c->off_x));  // flags + load matrix
+  LLEP_CUDA(cudaMalloc(&c->act, (size_t)rows * c->H * 2));
+  c->arena_rows = rows;
+  c->arena_foreign = foreign;
+  c->peer_base[c->rank] = c->arena;
+  if (c->P == 1) {
+    c->peers_ready = true;
+    return upload_peer_ptrs(c);
+  }
+  return LLEP_OK;
+}
+
+extern "C" {
+
+const char *llep_last_error(void) { return g_err; }
+const char *llep_version(void) { return "llep-b200 0.1 (sm_100a)"; }
+
+size_t llep_plan_bytes(int32_t n_experts, int32_t world_size) {
+  if (n_experts < 1 || world_size < 1) return 0;
+  return plan_layout(n_experts, world_size).bytes;
+}
+
+static llep_status plan_common(const int64_t *loads, int32_t N, int32_t P, const llep_params *p,
+                               void *out, bool force_ep) {
+  llep_status st;
+  if ((st = check_np(N, P)) != LLEP_OK) return st;
+  if ((st = check_params(p)) != LLEP_OK) return st;
+  if (!loads || !out) return invalid("null pointer");
+  int64_t S = 0;
+  for (int e = 0; e < N; ++e) {
+    if (loads[e] < 0) return invalid("negative load");
+    S += loads[e];
+  }
+  if (S > INT32_MAX) return invalid("total load exceeds int32 chunk bounds");
+  host_plan(loads, N, P, p, force_ep, reinterpret_cast<uint8_t *>(out));
+  return LLEP_OK;
+}
+
+llep_status llep_plan(const int64_t *loads, int32_t n_experts, int32_t world_size,
+                      const llep_params *params, void *plan_out) {
+  return plan_common(loads, n_experts, world_size, params, plan_out, false);
+}
+
+llep_status llep_plan_ep(const int64_t *loads, int32_t n_experts, int32_t world_size,
+                         const llep_params *params, void *plan_out) {
+  return plan_common(loads, n_experts, world_size, params, plan_out, true);
+}
+
+llep_status llep_plan_device(const int32_t *load_matrix, int32_t N, int32_t P,
+                             const llep_params *params, int32_t force_ep, void *plan_out,
+                             void *stream) {
+  llep_status st;
+  if ((st = check_np(N, P)) != LLEP_OK) return st;
+  if ((st = check_params(params)) != LLEP_OK) return st;
+  if (P > kMaxWorld) return invalid("device planner supports P <= 32");
+  if (!load_matrix || !plan_out) return invalid("null pointer");
+  LLEP_CUDA(launch_planner(load_matrix, N, P, params->alpha, params->min_chunk, params->lambda,
+                           force_ep, plan_out, (cudaStream_t)stream));
+  return LLEP_OK;
+}
+
+llep_status llep_context_create(const llep_shape *s, int32_t rank, int32_t device,
+                                int64_t max_tokens, llep_context **out) {
+  if (!s || !out) return invalid("null pointer");
+  llep_status st;
+  if ((st = check_np(s->n_experts, s->world_size)) != LLEP_OK) return st;
+  if (s->world_size > kMaxWorld) return invalid("P > 32 is not supported");
+  if (s->top_k < 1 || s->top_k > s->n_experts) return invalid("K not in [1, N]");
+  if (s->top_k > 32) return invalid("K > 32 is not supported");
+  if (s->d_model < 8 || s->d_ff < 8 || s->d_model % 8 || s->d_ff % 8)
+    return invalid("D and H must be positive multiples of 8");
+  if (rank < 0 || rank >= s->world_size) return invalid("rank out of range");
+  if (max_tokens < 0) return invalid("max_tokens < 0");
+  LLEP_CUDA(cudaSetDevice(device));
+  llep_context *c = new llep_context();
+  c->N = s->n_experts;
+  c->K = s->top_k;
+  c->D = s->d_model;
+  c->H = s->d_ff;
+  c->P = s->world_size;
+  c->M = c->N / c->P;
+  c->rank = rank;
+  c->device = device;
+  c->max_tokens = max_tokens;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  const int64_t slots = std::max<int64_t>(1, max_tokens * c->K);
+  const int64_t tiles = (slots + kTileSlots - 1) / kTileSlots;
+  auto A = [&](auto **p, size_t bytes) -> cudaError_t {
+    c->scratch_bytes += bytes;
+    return cudaMalloc(reinterpret_cast<void **>(p), bytes);
+  };
+  cudaError_t e = cudaSuccess;
+  const int N = c->N, P = c->P;
+  if (!e) e = A(&c->tile_cnt, sizeof(int32_t) * tiles * N);
+  if (!e) e = A(&c->tile_off, sizeof(int32_t) * tiles * N);
+  if (!e) e = A(&c->cnt, sizeof(int32_t) * N);
+  if (!e) e = A(&c->local_rank, sizeof(int32_t) * slots);
+  if (!e) e = A(&c->slot_dst, sizeof(int32_t) * 2 * slots);
+  if (!e) e = A(&c->err, sizeof(int32_t) * 4);
+  if (!e) e = A(&c->lm_local, sizeof(int32_t) * P * N);
+  if (!e) e = A(&c->rows_on, sizeof(int32_t) * N * P);
+  if (!e) e = A(&c->chunk_row, sizeof(int32_t) * N * (P + 1));
+  if (!e) e = A(&c->foreign_slot, sizeof(int32_t) * N * P);
+  if (!e) e = A(&c->dev_padded, sizeof(int32_t) * P);
+  if (!e) e = A(&c->dev_foreign, sizeof(int32_t) * P);
+  if (!e) e = A(&c->groups, sizeof(Group) * kMaxGroups);
+  if (!e) e = A(&c->summary, sizeof(LayoutSummary));
+  if (!e) e = A(&c->d_ptrs, sizeof(void *) * 4 * P);
+  if (!e) e = cudaMemset(c->err, 0, sizeof(int32_t) * 4);
+  if (!e) e = cudaMallocHost(&c->summary_host, sizeof(LayoutSummary));
+  if (!e) e = cudaMallocHost(&c->err_host, sizeof(int32_t) * 4);
+  if (!e) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  if (!e) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  if (!e) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  if (e) {
+    llep_context_destroy(c);
+    return cuda_status(e, "llep_context_create");
+  }
+  // initial arena: every rank's local slots, room for the balanced case
+  const int64_t rows0 = (max_tokens * c->K + (int64_t)c->M * kRowAlign);
+  if ((st = alloc_arena(c, rows0, 1)) != LLEP_OK) {
+    llep_context_destroy(c);
+    return st;
+  }
+  *out = c;
+  return LLEP_OK;
+}
+
+void llep_context_destroy(llep_context *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  close_peers(c);
+  void *ptrs[] = {c->tile_cnt, c->tile_off, c->cnt, c->local_rank, c->slot_dst, c->err,
+                  c->lm_local, c->rows_on, c->chunk_row, c->foreign_slot, c->dev_padded,
+                  c->dev_foreign, c->groups, c->summary, c->d_ptrs, c->act, c->arena};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  if (c->summary_host) cudaFreeHost(c->summary_host);
+  if (c->err_host) cudaFreeHost(c->err_host);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  delete c;
+}
+
+llep_status llep_context_ipc_handle(llep_context *c, void *handle64) {
+  if (!c || !handle64) return invalid("null pointer");
+  cudaIpcMemHandle_t h;
+  LLEP_CUDA(cudaIpcGetMemHandle(&h, c->arena));
+  static_assert(sizeof(h) == 64, "IPC handle is 64 bytes");
+  memcpy(handle64, &h, 64);
+  return LLEP_OK;
+}
+
+llep_status llep_context_open_peers(llep_context *c, const void *handles, int32_t n) {
+  if (!c || !handles) return invalid("null pointer");
+  if (n != c->P) return invalid("need one handle per rank");
+  close_peers(c);
+  for (int q = 0; q < c->P; ++q) {
+    if (q == c->rank) {
+      c->peer_base[q] = c->arena;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, reinterpret_cast<const uint8_t *>(handles) + 64 * q, 64);
+    void *p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      set_error("cudaIpcOpenMemHandle(rank %d): %s", q, cudaGetErrorString(e));
+      close_peers(c);
+      return LLEP_ERR_COMM;
+    }
+    c->peer_base[q] = reinterpret_cast<uint8_t *>(p);
+    c->peer_opened[q] = true;
+  }
+  c->peers_ready = true;
+  return upload_peer_ptrs(c);
+}
+
+llep_status llep_context_reserve(llep_context *c, int64_t rows, int32_t foreign) {
+  if (!c) return invalid("null context");
+  if (rows <= c->arena_rows && foreign <= c->arena_foreign && c->peers_ready) return LLEP_OK;
+  LLEP_CUDA(cudaSetDevice(c->device));
+  LLEP_CUDA(cudaDeviceSynchronize());
+  return alloc_arena(c, std::max(rows, c->arena_rows), std::max(foreign, c->arena_foreign));
+}
+
+int64_t llep_context_device_bytes(const llep_context *c) {
+  if (!c) return 0;
+  return (int64_t)(c->arena_bytes + c->scratch_bytes + (size_t)c->arena_rows * c->H * 2);
+}
+
+static uint32_t *const *peer_flags(llep_context *c) { return reinterpret_cast<uint32_t *const *>(c->d_ptrs); }
+static int32_t *const *peer_lm(llep_context *c) { return reinterpret_cast<int32_t *const *>(c->d_ptrs + c->P); }
+static uint16_t *const *peer_x(llep_context *c) { return reinterpret_cast<uint16_t *const *>(c->d_ptrs + 2 * c->P); }
+static float *const *peer_g(llep_context *c) { return reinterpret_cast<float *const *>(c->d_ptrs + 3 * c->P); }
+
+static llep_status barrier(llep_context *c, cudaStream_t s) {
+  if (c->P == 1) return LLEP_OK;
+  ++c->epoch;
+  LLEP_CUDA(launch_barrier(peer_flags(c), c->rank, c->P, c->epoch, c->err + 1, s));
+  return LLEP_OK;
+}
+
+static void fill_req(llep_context *c, llep_requirements *req) {
+  const LayoutSummary &s = *c->summary_host;
+  req->rows_needed = s.rows_needed;
+  req->foreign_needed = s.foreign_needed;
+  req->fits = (s.rows_needed <= c->arena_rows && s.foreign_needed <= c->arena_foreign) ? 1 : 0;
+  req->my_rows = s.my_rows;
+  req->my_groups = s.my_groups;
+  req->fallback_ep = s.fallback_ep;
+  req->force_count = s.force_count;
+  req->n_transfers = s.n_transfers;
+}
+
+static llep_status run_layout(llep_context *c, const void *plan, cudaStream_t s) {
+  LayoutArgs la;
+  la.plan = plan;
+  la.load_matrix = c->lm_local;
+  la.N = c->N;
+  la.P = c->P;
+  la.M = c->M;
+  la.rank = c->rank;
+  la.rows_on = c->rows_on;
+  la.chunk_row = c->chunk_row;
+  la.foreign_slot = c->foreign_slot;
+  la.groups = c->groups;
+  la.dev_padded = c->dev_padded;
+  la.dev_foreign = c->dev_foreign;
+  la.summary = c->summary;
+  LLEP_CUDA(launch_layout(la, s));
+  return LLEP_OK;
+}
+
+// one host synchronisation: plan blob + layout summary + error flags
+static llep_status read_back(llep_context *c, const void *plan, cudaStream_t s) {
+  const size_t pb = plan_layout(c->N, c->P).bytes;
+  c->plan_host.resize(pb);
+  LLEP_CUDA(cudaMemcpyAsync(c->plan_host.data(), plan, pb, cudaMemcpyDeviceToHost, s));
+  LLEP_CUDA(cudaMemcpyAsync(c->summary_host, c->summary, sizeof(LayoutSummary), cudaMemcpyDeviceToHost, s));
+  LLEP_CUDA(cudaMemcpyAsync(c->err_host, c->err, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, s));
+  LLEP_CUDA(cudaStreamSynchronize(s));
+  c->plan_dev_cached = plan;
+  if (c->err_host[0]) {
+    cudaMemsetAsync(c->err, 0, sizeof(int32_t) * 4, s);
+    set_error("router index outside [0, N)");
+    return LLEP_ERR_ROUTING;
+  }
+  if (c->err_host[1]) {
+    set_error("device barrier timed out (a peer did not arrive)");
+    return LLEP_ERR_COMM;
+  }
+  if (c->summary_host->error) {
+    set_error("plan inconsistent with the load matrix (chunk totals != l_e) or too many groups");
+    return LLEP_ERR_PLAN;
+  }
+  return LLEP_OK;
+}
+
+llep_status llep_prepare(llep_context *c, const int32_t *ids, int64_t B, const llep_params *prm,
+                         int32_t force_ep, void *plan_out, llep_requirements *req, void *stream) {
+  if (!c || !prm || !plan_out || (B > 0 && !ids)) return invalid("null pointer");
+  llep_status st;
+  if ((st = check_params(prm)) != LLEP_OK) return st;
+  if (B < 0 || B > c->max_tokens) return invalid("n_tokens outside [0, max_tokens]");
+  if (c->P > 1 && !c->peers_ready) {
+    set_error("peers not opened (llep_context_open_peers)");
+    return LLEP_ERR_COMM;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int N = c->N, P = c->P;
+  const int64_t slots = B * c->K;
+  const int n_tiles = (int)((slots + kTileSlots - 1) / kTileSlots);
+  // a1: per-tile histogram + scan -> counts row; a3: stable local ranks
+  LLEP_CUDA(launch_tile_count(ids, slots, N, c->tile_cnt, c->err, s));
+  if (n_tiles > 0) {
+    LLEP_CUDA(launch_tile_scan(c->tile_cnt, n_tiles, N, c->tile_off, c->cnt, s));
+  } else {
+    LLEP_CUDA(cudaMemsetAsync(c->cnt, 0, sizeof(int32_t) * N, s));
+  }
+  LLEP_CUDA(launch_local_rank(ids, slots, N, c->tile_off, c->local_rank, s));
+  // a2: push the counts row into every rank's load matrix, barrier, keep a local copy
+  LLEP_CUDA(launch_push_counts(c->cnt, N, c->rank, P, peer_lm(c), s));
+  if ((st = barrier(c, s)) != LLEP_OK) return st;
+  LLEP_CUDA(cudaMemcpyAsync(c->lm_local, c->arena + c->off_lm, sizeof(int32_t) * P * N,
+                            cudaMemcpyDeviceToDevice, s));
+  // a4: planner; a5: layout
+  LLEP_CUDA(launch_planner(c->lm_local, N, P, prm->alpha, prm->min_chunk, prm->lambda, force_ep,
+                           plan_out, s));
+  if ((st = run_layout(c, plan_out, s)) != LLEP_OK) return st;
+  if ((st = read_back(c, plan_out, s)) != LLEP_OK) return st;
+  c->prepared_tokens = B;
+  if (req) fill_req(c, req);
+  return LLEP_OK;
+}
+
+llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *ids,
+                             const float *topk_w, int64_t B, const uint16_t *w13,
+                             const uint16_t *w2, const void *plan, uint16_t *out, void *stream) {
+  if (!c || !plan || !w13 || !w2 || (B > 0 && (!x || !ids || !topk_w || !out)))
+    return invalid("null pointer");
+  if (B != c->prepared_tokens) return invalid("n_tokens differs from the last llep_prepare");
+  cudaStream_t s = (cudaStream_t)stream;
+  llep_status st;
+  if (plan != c->plan_dev_cached) {
+    if ((st = run_layout(c, plan, s)) != LLEP_OK) return st;
+    if ((st = read_back(c, plan, s)) != LLEP_OK) return st;
+  }
+  const LayoutSummary &sum = *c->summary_host;
+  if (sum.rows_needed > c->arena_rows || sum.foreign_needed > c->arena_foreign) {
+    set_error("plan needs %lld rows / %d foreign experts, arena holds %lld / %d: call "
+              "llep_context_reserve", (long long)sum.rows_needed, sum.foreign_needed,
+              (long long)c->arena_rows, c->arena_foreign);
+    return LLEP_ERR_PLAN;
+  }
+  const int N = c->N, P = c->P, M = c->M, D = c->D, H = c->H;
+  // a7: weight migration, pushed by the native device on a side stream (copy engines)
+  const PlanLayout L = plan_layout(N, P);
+  const uint8_t *ph = c->plan_host.data();
+  const uint8_t *replica = ph + L.off_replica;
+  const size_t w13_bytes = (size_t)2 * H * D * 2, w2_bytes = (size_t)D * H * 2;
+  bool any_copy = false;
+  for (int d = 0; d < P && P > 1; ++d) {
+    if (d == c->rank) continue;
+    int f = 0;
+    for (int e = 0; e < N; ++e) {
+      if (!replica[(size_t)e * P + d]) continue;
+      if (e / M == c->rank) {
+        if (!any_copy) {
+          LLEP_CUDA(cudaEventRecord(c->ev_fork, s));
+          LLEP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+          any_copy = true;
+        }
+        const int el = e - c->rank * M;
+        LLEP_CUDA(cudaMemcpyAsync(c->peer_base[d] + c->off_w13 + (size_t)f * w13_bytes,
+                                  w13 + (size_t)el * 2 * H * D, w13_bytes, cudaMemcpyDeviceToDevice,
+                                  c->side));
+        LLEP_CUDA(cudaMemcpyAsync(c->peer_base[d] + c->off_w2 + (size_t)f * w2_bytes,
+                                  w2 + (size_t)el * D * H, w2_bytes, cudaMemcpyDeviceToDevice,
+                                  c->side));
+      }
+      ++f;
+    }
+  }
+  if (any_copy) LLEP_CUDA(cudaEventRecord(c->ev_join, c->side));
+  // a6: dispatch (gather-on-send into every destination's receive rows)
+  DispatchArgs da;
+  da.x = x;
+  da.ids = ids;
+  da.w = topk_w;
+  da.local_rank = c->local_rank;
+  da.load_matrix = c->lm_local;
+  da.plan = plan;
+  da.chunk_row = c->chunk_row;
+  da.B = B;
+  da.K = c->K;
+  da.D = D;
+  da.N = N;
+  da.P = P;
+  da.rank = c->rank;
+  da.peer_x = peer_x(c);
+  da.peer_g = peer_g(c);
+  da.slot_dst = c->slot_dst;
+  LLEP_CUDA(launch_dispatch(da, s));
+  if (any_copy) LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+  if ((st = barrier(c, s)) != LLEP_OK) return st;
+  // a8: GEMM1 + SwiGLU   X [rows, D] -> A [rows, H]
+  uint16_t *X = reinterpret_cast<uint16_t *>(c->arena + c->off_x);
+  GemmArgs g1;
+  g1.mode = 0;
+  g1.a = X;
+  g1.a_rows = c->arena_rows;
+  g1.kdim = D;
+  g1.w_native = w13;
+  g1.n_native = M;
+  g1.w_foreign = reinterpret_cast<const uint16_t *>(c->arena + c->off_w13);
+  g1.n_foreign = c->arena_foreign;
+  g1.nout = H;
+  g1.groups = c->groups;
+  g1.n_groups_dev = nullptr;
+  g1.n_groups_host = sum.my_groups;
+  g1.gate = nullptr;
+  g1.out = c->act;
+  g1.num_sms = c->num_sms;
+  if (sum.my_groups > 0 && (st = run_grouped_gemm(g1, s)) != LLEP_OK) return st;
+  // a9: GEMM2 + gate   A [rows, H] -> Y [rows, D]  (Y reuses X's rows: X is dead after GEMM1)
+  GemmArgs g2 = g1;
+  g2.mode = 1;
+  g2.a = c->act;
+  g2.kdim = H;
+  g2.w_native = w2;
+  g2.w_foreign = reinterpret_cast<const uint16_t *>(c->arena + c->off_w2);
+  g2.nout = D;
+  g2.gate = reinterpret_cast<const float *>(c->arena + c->off_g);
+  g2.out = X;
+  if (sum.my_groups > 0 && (st = run_grouped_gemm(g2, s)) != LLEP_OK) return st;
+  if ((st = barrier(c, s)) != LLEP_OK) return st;
+  // a10: combine (pull each slot's Y row from its device, K-sum in slot order)
+  CombineArgs ca;
+  ca.slot_dst = c->slot_dst;
+  ca.peer_y = peer_x(c);
+  ca.B = B;
+  ca.K = c->K;
+  ca.D = D;
+  ca.out = out;
+  LLEP_CUDA(launch_combine(ca, s));
+  return LLEP_OK;
+}
+
+llep_status llep_debug_copy(llep_context *c, int32_t what, void *dst, int64_t n, void *stream) {
+  if (!c || !dst) return invalid("null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const void *src = nullptr;
+  size_t esz = 4, avail = 0;
+  const int64_t slots = std::max<int64_t>(0, c->prepared_tokens) * c->K;
+  switch (what) {
+    case LLEP_DBG_LOAD_MATRIX: src = c->lm_local; avail = (size_t)c->P * c->N; break;
+    case LLEP_DBG_SLOT_DST: src = c->slot_dst; avail = 2 * slots; break;
+    case LLEP_DBG_GROUPS: src = c->groups; avail = (size_t)kMaxGroups * 8; break;
+    case LLEP_DBG_RECV_X: src = c->arena + c->off_x; esz = 2; avail = (size_t)c->arena_rows * c->D; break;
+    case LLEP_DBG_Y: src = c->arena + c->off_x; esz = 2; avail = (size_t)c->arena_rows * c->D; break;
+    case LLEP_DBG_ACT: src = c->act; esz = 2; avail = (size_t)c->arena_rows * c->H; break;
+    case LLEP_DBG_LOCAL_RANK: src = c->local_rank; avail = slots; break;
+    case LLEP_DBG_RECV_G: src = c->arena + c->off_g; avail = c->arena_rows; break;
+    default: return invalid("unknown debug buffer");
+  }
+  if (n < 0 || (size_t)n > avail) return invalid("n_elems exceeds the buffer");
+  LLEP_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * esz, cudaMemcpyDeviceToDevice, s));
+  return LLEP_OK;
+}
+
+llep_status llep_grouped_gemm(int32_t mode, const uint16_t *a, int64_t rows, int32_t kdim,
+                              const uint16_t *w, int32_t n_weights, int32_t nout,
+                              const int32_t *groups, int32_t n_groups, const float *gate,
+                              uint16_t *out, void *stream) {
+  if (!a || !w || !groups || !out || (mode == 1 && !gate)) return invalid("null pointer");
+  if (mode != 0 && mode != 1) return invalid("mode must be 0 or 1");
+  if (n_groups < 0 || n_groups > kMaxGroups) return invalid("n_groups out of range");
+  std::vector<Group> g(std::max(n_groups, 1));
+  int mb = 0;
+  for (int i = 0; i < n_groups; ++i) {
+    const int32_t *q = groups + 4 * i;
+    if (q[0] < 0 || q[0] >= n_weights) return invalid("group expert out of range");
+    if (q[1] % kRowAlign || q[2] < 1 || q[1] + (int64_t)q[2] > rows)
+      return invalid("group rows must start 128-aligned, be nonempty and fit in `rows`");
+    if (i > 0 && q[1] < g[i - 1].row_base + ((g[i - 1].n_rows + kRowAlign - 1) / kRowAlign) * kRowAlign)
+      return invalid("groups must be in increasing, non-overlapping row order");
+    g[i] = Group{q[0], q[0], q[1], q[2], mb, {0, 0, 0}};
+    mb += (q[2] + kRowAlign - 1) / kRowAlign;
+    // mblk_start counts only this group's blocks: rows between groups are skipped
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  Group *dg = nullptr;
+  LLEP_CUDA(cudaMallocAsync(&dg, sizeof(Group) * g.size(), s));
+  LLEP_CUDA(cudaMemcpyAsync(dg, g.data(), sizeof(Group) * g.size(), cudaMemcpyHostToDevice, s));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  GemmArgs ga;
+  ga.mode = mode;
+  ga.a = a;
+  ga.a_rows = rows;
+  ga.kdim = kdim;
+  ga.w_native = w;
+  ga.n_native = n_weights;
+  ga.w_foreign = nullptr;
+  ga.n_foreign = 0;
+  ga.nout = nout;
+  ga.groups = dg;
+  ga.n_groups_dev = nullptr;
+  ga.n_groups_host = n_groups;
+  ga.gate = gate;
+  ga.out = out;
+  ga.num_sms = sms;
+  llep_status st = n_groups > 0 ? run_grouped_gemm(ga, s) : LLEP_OK;
+  cudaFreeAsync(dg, s);
+  return st;
+}
+
+}  // extern "C"

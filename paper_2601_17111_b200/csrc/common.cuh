@@ -1,0 +1,145 @@
+// Internal declarations shared by the LLEP CUDA translation units (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "llep.h"
+
+namespace llep {
+
+constexpr int kMaxWorld = 32;     // device planner keeps one device per lane
+constexpr int kRowAlign = 128;    // group row bases are aligned to the GEMM M tile
+constexpr int kTileSlots = 1024;  // slots per histogram / local-rank tile
+constexpr int kMaxGroups = 1024;  // expert groups one rank may compute
+
+void set_error(const char *fmt, ...);
+llep_status cuda_status(cudaError_t e, const char *what);
+
+#define LLEP_CUDA(call)                                                    \
+  do {                                                                     \
+    cudaError_t _e = (call);                                               \
+    if (_e != cudaSuccess) return ::llep::cuda_status(_e, #call);          \
+  } while (0)
+
+// Plan blob field offsets (see llep.h "plan blob").
+struct PlanLayout {
+  int32_t off_assigned, off_n_chunks, off_chunks, off_replica;
+  size_t bytes;
+};
+__host__ __device__ inline size_t align8(size_t x) { return (x + 7) & ~size_t(7); }
+__host__ __device__ inline PlanLayout plan_layout(int32_t N, int32_t P) {
+  PlanLayout L;
+  size_t off = align8(sizeof(llep_plan_header));
+  L.off_assigned = (int32_t)off;
+  off = align8(off + sizeof(int64_t) * P);
+  L.off_n_chunks = (int32_t)off;
+  off = align8(off + sizeof(int32_t) * N);
+  L.off_chunks = (int32_t)off;
+  off = align8(off + sizeof(llep_chunk) * (size_t)N * (P + 1));
+  L.off_replica = (int32_t)off;
+  off = align8(off + (size_t)N * P);
+  L.bytes = off;
+  return L;
+}
+
+// Group table entry (8 int32) of one expert group a device computes.
+struct Group {
+  int32_t expert;      // global expert id
+  int32_t wslot;       // >= 0: native slot (e - rank*M);  < 0: foreign slot f = -1 - wslot
+  int32_t row_base;    // first receive row (multiple of kRowAlign)
+  int32_t n_rows;      // rows of this expert on this device
+  int32_t mblk_start;  // prefix sum of ceil(n_rows / 128) over earlier groups
+  int32_t pad[3];
+};
+
+// Summary written by the layout kernel, read back once by the host.
+struct LayoutSummary {
+  int64_t rows_needed;   // max_d padded rows
+  int64_t my_rows;       // g_a[rank]
+  int64_t my_padded;     // padded rows of this rank
+  int32_t foreign_needed;
+  int32_t my_groups;
+  int32_t my_mblocks;
+  int32_t fallback_ep, force_count, n_transfers;
+  int32_t error;         // nonzero: plan/load inconsistency
+  int32_t pad;
+};
+
+// Device workspace pointers of the layout step (rank-local).
+struct LayoutArgs {
+  const void *plan;
+  const int32_t *load_matrix;  // [P, N]
+  int32_t N, P, M, rank;
+  int32_t *rows_on;            // [N*P] rows of e on d
+  int32_t *chunk_row;          // [N*(P+1)] destination row of each chunk's first token
+  int32_t *foreign_slot;       // [N*P] foreign slot of e on d, -1 if none
+  Group *groups;               // [kMaxGroups] this rank's groups
+  int32_t *dev_padded;         // [P] padded rows per device
+  int32_t *dev_foreign;        // [P] |S_d|
+  LayoutSummary *summary;
+};
+
+// kernel launchers (route.cu / plan.cu / gemm.cu)
+cudaError_t launch_tile_count(const int32_t *ids, int64_t n_slots, int32_t N, int32_t *tile_cnt,
+                              int32_t *err, cudaStream_t s);
+cudaError_t launch_tile_scan(const int32_t *tile_cnt, int32_t n_tiles, int32_t N, int32_t *tile_off,
+                             int32_t *cnt_out, cudaStream_t s);
+cudaError_t launch_local_rank(const int32_t *ids, int64_t n_slots, int32_t N, const int32_t *tile_off,
+                              int32_t *local_rank, cudaStream_t s);
+cudaError_t launch_push_counts(const int32_t *cnt, int32_t N, int32_t rank, int32_t P,
+                               int32_t *const *peer_lm, cudaStream_t s);
+cudaError_t launch_barrier(uint32_t *const *peer_flags, int32_t rank, int32_t P, uint32_t epoch,
+                           int32_t *err, cudaStream_t s);
+cudaError_t launch_planner(const int32_t *load_matrix, int32_t N, int32_t P, double alpha,
+                           int64_t min_chunk, double lambda, int32_t force_ep, void *plan,
+                           cudaStream_t s);
+cudaError_t launch_layout(const LayoutArgs &a, cudaStream_t s);
+
+struct DispatchArgs {
+  const uint16_t *x;        // [B, D]
+  const int32_t *ids;       // [B, K]
+  const float *w;           // [B, K]
+  const int32_t *local_rank;
+  const int32_t *load_matrix;
+  const void *plan;
+  const int32_t *chunk_row;
+  int64_t B;
+  int32_t K, D, N, P, rank;
+  uint16_t *const *peer_x;  // [P] receive rows base of each device (peer-mapped)
+  float *const *peer_g;     // [P]
+  int32_t *slot_dst;        // [2*B*K] (device, row)
+};
+cudaError_t launch_dispatch(const DispatchArgs &a, cudaStream_t s);
+
+struct CombineArgs {
+  const int32_t *slot_dst;
+  const uint16_t *const *peer_y;  // [P]
+  int64_t B;
+  int32_t K, D;
+  uint16_t *out;
+};
+cudaError_t launch_combine(const CombineArgs &a, cudaStream_t s);
+
+// grouped GEMM (gemm.cu).  mode 0: SwiGLU epilogue; mode 1: gate-scale epilogue.
+struct GemmArgs {
+  int32_t mode;
+  const uint16_t *a;         // [rows, kdim]
+  int64_t a_rows;
+  int32_t kdim;
+  const uint16_t *w_native;  // [n_native * wrows, kdim]
+  int32_t n_native;
+  const uint16_t *w_foreign; // [n_foreign * wrows, kdim]
+  int32_t n_foreign;
+  int32_t nout;              // output columns: H (mode 0) or D (mode 1)
+  const Group *groups;       // device
+  const int32_t *n_groups_dev;  // device int (may be nullptr -> n_groups_host)
+  int32_t n_groups_host;
+  const float *gate;         // [rows] (mode 1)
+  uint16_t *out;             // [rows, nout]
+  int32_t num_sms;
+};
+llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s);
+
+}  // namespace llep

@@ -1,0 +1,425 @@
+// Grouped expert GEMMs on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+// The expert FFN is the dense part of the layer (a8/a9; T_local of §3.2).  The paper
+// ran it as a cuBLAS loop or a Triton grouped GEMM (F-gemm P:1127); here ONE persistent
+// kernel per projection walks every (group, 128-row block, N tile) of this device:
+//   warp 0      TMA producer: A tile [128 x 64] + B tile [BN x 64] per stage, 128-byte swizzle
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16 steps)
+//   warps 2-5   epilogue: tcgen05.ld of the fp32 accumulator, fused activation, bf16 stores
+// Accumulators are double-buffered in TMEM (2 x 256 columns) so the epilogue of tile i overlaps
+// the MMAs of tile i+1.  Epilogues:
+//   mode 0 (GEMM1 + SwiGLU): the B tile stacks BN/2 rows of W_gate over the matching BN/2 rows
+//     of W_up (two TMA boxes), so one accumulator tile holds both halves of each output column:
+//     A[r, n] = silu(acc[r, n]) * acc[r, BN/2 + n]   (no [n, 2H] intermediate in HBM)
+//   mode 1 (GEMM2 + gate): Y[r, n] = gate[r] * acc[r, n]   (Ĥ = Ĝ ⊙ B̂W)
+// Groups start at 128-aligned rows, so an M tile never straddles two experts; rows past a
+// group's end are computed on padding and masked at the store.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace llep {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;                 // 64 bf16 = 128 bytes = one swizzle row
+constexpr int kGemmThreads = 192;
+constexpr int kAccCols = 256;          // TMEM columns per accumulator buffer
+constexpr int kSmemBudget = 227 * 1024;
+
+struct GemmParams {
+  CUtensorMap tmA;     // activations [rows, kdim]
+  CUtensorMap tmW0;    // native weights [n_native * wrows, kdim]
+  CUtensorMap tmW1;    // foreign weights [n_foreign * wrows, kdim]
+  const Group *groups;
+  const int32_t *n_groups_dev;
+  int32_t n_groups_host;
+  int32_t kdim, nout, wrows, n_ntiles, wup_off;
+  const float *gate;
+  __nv_bfloat16 *out;
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int EXTRA = 1024 + 256 + (kMaxGroups + 1) * 4;
+  static constexpr int STAGES_RAW = (kSmemBudget - EXTRA) / STAGE;
+  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+  static constexpr int SMEM = STAGES * STAGE + EXTRA;
+  static_assert(B_BYTES % 1024 == 0, "B tile must keep 1024-byte swizzle alignment");
+  static_assert(STAGES >= 2, "pipeline too shallow");
+};
+
+// ------------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+// D[tmem] (+)= A[smem] x B[smem]^T, bf16 inputs, fp32 accumulator (kind::f16)
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float *v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);          // start address
+  d |= (uint64_t)1 << 16;                          // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                // stride byte offset between 8-row atoms
+  d |= (uint64_t)1 << 46;                          // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                          // layout: SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: bf16 A/B, fp32 D, both K-major, M=128, N=BN
+template <int BN>
+__device__ __forceinline__ uint32_t instr_desc() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
+
+struct TileInfo {
+  int row0, row_end, nb, wslot, valid;
+};
+
+__device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int *s_mblk,
+                                                int n_groups, const Group *groups) {
+  TileInfo ti;
+  const int mb = t / n_ntiles;
+  ti.nb = t - mb * n_ntiles;
+  int lo = 0, hi = n_groups - 1;  // last g with s_mblk[g] <= mb
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_mblk[mid] <= mb) lo = mid;
+    else hi = mid - 1;
+  }
+  const Group g = groups[lo];
+  ti.row0 = g.row_base + (mb - s_mblk[lo]) * BM;
+  ti.row_end = g.row_base + g.n_rows;
+  ti.wslot = g.wslot;
+  ti.valid = 1;
+  return ti;
+}
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __grid_constant__ GemmParams p) {
+  using C = Cfg<BN>;
+  constexpr int S = C::STAGES;
+  constexpr int BNO = MODE == 0 ? BN / 2 : BN;   // output columns per tile
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + S * C::A_BYTES;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S * C::STAGE);
+  uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+  int *s_mblk = reinterpret_cast<int *>(smem + S * C::STAGE + 256);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_groups = p.n_groups_dev ? *p.n_groups_dev : p.n_groups_host;
+  for (int g = threadIdx.x; g < n_groups; g += kGemmThreads) s_mblk[g] = p.groups[g].mblk_start;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(smem_u32(full + i), 1);
+      mbar_init(smem_u32(empty + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(tfull + i), 1);
+      mbar_init(smem_u32(tempty + i), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmW0)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmW1)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(2 * kAccCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  int total_tiles = 0;
+  if (n_groups > 0) {
+    const Group last = p.groups[n_groups - 1];
+    total_tiles = (last.mblk_start + (last.n_rows + BM - 1) / BM) * p.n_ntiles;
+  }
+  const int nk = (p.kdim + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const TileInfo ti = decode_tile(t, p.n_ntiles, s_mblk, n_groups, p.groups);
+        const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
+        const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(smem_u32(empty + stage), phase ^ 1);
+          const uint32_t fb = smem_u32(full + stage);
+          mbar_expect_tx(fb, C::STAGE);
+          tma_load_2d(smem_u32(sA + stage * C::A_BYTES), &p.tmA, fb, kb * BK, ti.row0);
+          if (MODE == 0) {
+            tma_load_2d(smem_u32(sB + stage * C::B_BYTES), wm, fb, kb * BK, wbase);
+            tma_load_2d(smem_u32(sB + stage * C::B_BYTES + (BN / 2) * BK * 2), wm, fb, kb * BK,
+                        wbase + p.wup_off);
+          } else {
+            tma_load_2d(smem_u32(sB + stage * C::B_BYTES), wm, fb, kb * BK, wbase);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      const uint32_t idesc = instr_desc<BN>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(smem_u32(tempty + acc), aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(smem_u32(full + stage), phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            tc_mma(d_tmem, smem_desc(a0 + kk * 32), smem_desc(b0 + kk * 32), idesc,
+                   (kb | kk) != 0);
+          tc_commit(smem_u32(empty + stage));  // frees the smem stage when these MMAs finish
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(smem_u32(tfull + acc));      // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue (warps 2-5)
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int it = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      const TileInfo ti = decode_tile(t, p.n_ntiles, s_mblk, n_groups, p.groups);
+      mbar_wait(smem_u32(tfull + acc), aphase);
+      tc_fence_after();
+      const int row = ti.row0 + q * 32 + lane;
+      const bool row_ok = row < ti.row_end;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
+      const int col0 = ti.nb * BNO;
+      if (MODE == 0) {
+        __nv_bfloat16 *orow = p.out + (size_t)row * p.nout + col0;
+#pragma unroll 1
+        for (int j = 0; j < BNO; j += 8) {
+          float g[8], u[8];
+          tmem_ld8(taddr + j, g);
+          tmem_ld8(taddr + BNO + j, u);
+          tmem_ld_wait();
+          if (row_ok && col0 + j < p.nout) {
+            uint4 o;
+            __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float a0 = g[2 * i] / (1.f + __expf(-g[2 * i])) * u[2 * i];
+              const float a1 = g[2 * i + 1] / (1.f + __expf(-g[2 * i + 1])) * u[2 * i + 1];
+              h[i] = __floats2bfloat162_rn(a0, a1);
+            }
+            *reinterpret_cast<uint4 *>(orow + j) = o;
+          }
+        }
+      } else {
+        const float gs = row_ok ? p.gate[row] : 0.f;
+        __nv_bfloat16 *orow = p.out + (size_t)row * p.nout + col0;
+#pragma unroll 1
+        for (int j = 0; j < BNO; j += 8) {
+          float v[8];
+          tmem_ld8(taddr + j, v);
+          tmem_ld_wait();
+          if (row_ok && col0 + j < p.nout) {
+            uint4 o;
+            __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(gs * v[2 * i], gs * v[2 * i + 1]);
+            *reinterpret_cast<uint4 *>(orow + j) = o;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(2 * kAccCols)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap *m, const void *ptr, int64_t rows, int32_t kdim, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  if (rows < 1) rows = 1;
+  cuuint64_t dims[2] = {(cuuint64_t)kdim, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kdim * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int MODE>
+llep_status launch(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
+  using C = Cfg<BN>;
+  auto kern = grouped_gemm_kernel<BN, MODE>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    LLEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  const int box_w = MODE == 0 ? BN / 2 : BN;
+  const int wrows = MODE == 0 ? 2 * g.nout : g.nout;
+  if (!make_map(&prm.tmA, g.a, g.a_rows, g.kdim, BM) ||
+      !make_map(&prm.tmW0, g.w_native, (int64_t)g.n_native * wrows, g.kdim, box_w) ||
+      !make_map(&prm.tmW1, g.w_foreign ? g.w_foreign : g.w_native,
+                (int64_t)(g.w_foreign ? g.n_foreign : g.n_native) * wrows, g.kdim, box_w)) {
+    set_error("cuTensorMapEncodeTiled failed (alignment: kdim %% 8 == 0, 16-byte aligned bases)");
+    return LLEP_ERR_CUDA;
+  }
+  prm.wrows = wrows;
+  prm.wup_off = MODE == 0 ? g.nout : 0;
+  prm.n_ntiles = (g.nout + box_w - 1) / box_w;
+  grouped_gemm_kernel<BN, MODE><<<g.num_sms, kGemmThreads, C::SMEM, s>>>(prm);
+  LLEP_CUDA(cudaGetLastError());
+  return LLEP_OK;
+}
+
+}  // namespace
+
+llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
+  if (g.kdim % 8 != 0 || g.nout % 8 != 0) {
+    set_error("grouped GEMM needs kdim %% 8 == 0 and nout %% 8 == 0");
+    return LLEP_ERR_INVALID;
+  }
+  GemmParams prm;
+  memset(&prm, 0, sizeof(prm));
+  prm.groups = g.groups;
+  prm.n_groups_dev = g.n_groups_dev;
+  prm.n_groups_host = g.n_groups_host;
+  prm.kdim = g.kdim;
+  prm.nout = g.nout;
+  prm.gate = g.gate;
+  prm.out = reinterpret_cast<__nv_bfloat16 *>(g.out);
+  // tile width: widest instantiated N that divides the output (else masked tail tiles)
+  if (g.mode == 0) {
+    if (g.nout % 128 == 0) return launch<256, 0>(g, prm, s);
+    if (g.nout % 120 == 0) return launch<240, 0>(g, prm, s);
+    if (g.nout % 96 == 0) return launch<192, 0>(g, prm, s);
+    return launch<256, 0>(g, prm, s);
+  }
+  if (g.nout % 256 == 0) return launch<256, 1>(g, prm, s);
+  if (g.nout % 240 == 0) return launch<240, 1>(g, prm, s);
+  if (g.nout % 192 == 0) return launch<192, 1>(g, prm, s);
+  return launch<256, 1>(g, prm, s);
+}
+
+}  // namespace llep

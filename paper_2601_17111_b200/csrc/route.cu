@@ -1,0 +1,314 @@
+// Routing-side kernels of the LLEP layer: load histogram (a1), load exchange + device barrier
+// (a2), stable per-expert local ranks (a3), dispatch (a6) and combine (a10).
+//
+// The paper re-indexes with sort + index_select of the K-repeated tokens (Alg. 1/4, P:299-303,
+// P:542-544) and calls that step memory-intensive.  Here the permutation is never
+// materialised: a counting sort gives every flat slot j = t*K+k its stable rank r_j among this
+// rank's slots of the same expert (P:282's order), dispatch turns (e, Σ_{q<p} C[q][e] + r_j)
+// into a (device, row) through the replicated plan and copies the token row straight from the
+// unsorted x into the destination's receive rows ("direct All-to-All on unsorted tensors",
+// P:578), and combine pulls each slot's output row back and sums over K in slot order.
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace llep {
+
+namespace {
+
+// ------------------------------------------------------------------------------ a1: histogram
+constexpr int kCountThreads = 256;
+
+__global__ void __launch_bounds__(kCountThreads) tile_count_kernel(
+    const int32_t *__restrict__ ids, int64_t n_slots, int N, int32_t *__restrict__ tile_cnt,
+    int32_t *__restrict__ err) {
+  extern __shared__ int32_t hist[];
+  for (int e = threadIdx.x; e < N; e += kCountThreads) hist[e] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kTileSlots;
+  const int64_t end = min(base + kTileSlots, n_slots);
+  int bad = 0;
+  for (int64_t j = base + threadIdx.x; j < end; j += kCountThreads) {
+    const int e = ids[j];
+    if (e >= 0 && e < N) atomicAdd(&hist[e], 1);
+    else bad = 1;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, 1);
+  for (int e = threadIdx.x; e < N; e += kCountThreads)
+    tile_cnt[(size_t)blockIdx.x * N + e] = hist[e];
+}
+
+// exclusive scan over tiles per expert -> tile offsets; totals = this rank's counts row
+__global__ void tile_scan_kernel(const int32_t *__restrict__ tile_cnt, int n_tiles, int N,
+                                 int32_t *__restrict__ tile_off, int32_t *__restrict__ cnt) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N) return;
+  int run = 0;
+  for (int t = 0; t < n_tiles; ++t) {
+    const int v = tile_cnt[(size_t)t * N + e];
+    tile_off[(size_t)t * N + e] = run;
+    run += v;
+  }
+  cnt[e] = run;
+}
+
+// ----------------------------------------------------------------- a3: stable local ranks r_j
+// One CTA per 1024-slot tile, 8 warps x 128 consecutive slots.  Pass 1 counts per warp with
+// __match_any_sync (one smem update per distinct expert per 32 slots), an exclusive scan over
+// the warps seeds each warp's counters with the tile offset, pass 2 re-walks the slots in order.
+constexpr int kRankWarps = 8;
+constexpr int kRankThreads = kRankWarps * 32;
+constexpr int kSlotsPerWarp = kTileSlots / kRankWarps;
+
+__global__ void __launch_bounds__(kRankThreads) local_rank_kernel(
+    const int32_t *__restrict__ ids, int64_t n_slots, int N, const int32_t *__restrict__ tile_off,
+    int32_t *__restrict__ local_rank) {
+  extern __shared__ int32_t wcnt[];  // [kRankWarps][N]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kRankWarps * N; i += kRankThreads) wcnt[i] = 0;
+  __syncthreads();
+  const int64_t wbase = (int64_t)blockIdx.x * kTileSlots + (int64_t)warp * kSlotsPerWarp;
+  int32_t *mine = wcnt + warp * N;
+  for (int i = 0; i < kSlotsPerWarp; i += 32) {
+    const int64_t j = wbase + i + lane;
+    int e = j < n_slots ? ids[j] : -1;
+    if (e >= N) e = -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    if (e >= 0 && lane == __ffs(peers) - 1) mine[e] += __popc(peers);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < N; e += kRankThreads) {
+    int run = tile_off[(size_t)blockIdx.x * N + e];
+    for (int w = 0; w < kRankWarps; ++w) {
+      const int v = wcnt[w * N + e];
+      wcnt[w * N + e] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  for (int i = 0; i < kSlotsPerWarp; i += 32) {
+    const int64_t j = wbase + i + lane;
+    int e = j < n_slots ? ids[j] : -1;
+    if (e >= N) e = -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int r = __popc(peers & ((1u << lane) - 1u));
+    int base = 0;
+    if (e >= 0) base = mine[e];
+    __syncwarp();
+    if (j < n_slots) local_rank[j] = e >= 0 ? base + r : -1;
+    if (e >= 0 && lane == __ffs(peers) - 1) mine[e] = base + __popc(peers);
+    __syncwarp();
+  }
+}
+
+// ----------------------------------------------------------------- a2: exchange + barrier
+__global__ void push_counts_kernel(const int32_t *__restrict__ cnt, int N, int rank, int P,
+                                   int32_t *const *__restrict__ peer_lm) {
+  for (int q = blockIdx.x; q < P; q += gridDim.x) {
+    int32_t *dst = peer_lm[q] + (size_t)rank * N;
+    for (int e = threadIdx.x; e < N; e += blockDim.x) dst[e] = cnt[e];
+  }
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Every rank writes `epoch` into slot [rank] of every peer's flag array, then waits until all
+// of its own slots reach `epoch`.  Writes of earlier kernels on this stream happen-before the
+// release (stream order + cumulativity), so after the acquire every peer's earlier stores to
+// this rank's arena are visible to the kernels that follow.  Bounded spin -> COMM error.
+__global__ void barrier_kernel(uint32_t *const *__restrict__ peer_flags, int rank, int P,
+                               uint32_t epoch, int32_t *__restrict__ err) {
+  const int q = threadIdx.x;
+  if (q < P) {
+    __threadfence_system();
+    st_release_sys(peer_flags[q] + rank, epoch);
+    const uint32_t *mine = peer_flags[rank] + q;
+    const long long t0 = clock64();
+    long long spins = 0;
+    while ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
+      if (((++spins) & 1023) == 0 && clock64() - t0 > 40000000000LL) {  // ~20 s
+        atomicOr(err, 4);
+        break;
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- a6: dispatch
+// One warp per token: lanes k < K resolve slot (t,k) to its (device, row); then the warp streams
+// x[t] once (16-byte loads) and stores it to each of the K destinations (peer-mapped rows).
+constexpr int kDispatchWarps = 8;
+
+__global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_kernel(DispatchArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * kDispatchWarps + (threadIdx.x >> 5);
+  if (t >= a.B) return;
+  const int K = a.K, N = a.N, P = a.P, MC = P + 1;
+  const uint8_t *plan = reinterpret_cast<const uint8_t *>(a.plan);
+  const PlanLayout L = plan_layout(N, P);
+  const int32_t *n_chunks = reinterpret_cast<const int32_t *>(plan + L.off_n_chunks);
+  const llep_chunk *chunks = reinterpret_cast<const llep_chunk *>(plan + L.off_chunks);
+  int dev = -1, row = 0;
+  if (lane < K) {
+    const int64_t j = t * K + lane;
+    const int e = a.ids[j];
+    if (e >= 0 && e < N) {
+      int g = a.local_rank[j];
+      for (int q = 0; q < a.rank; ++q) g += a.load_matrix[(size_t)q * N + e];  // rank-major (R11)
+      const int nc = n_chunks[e];
+      for (int c = 0; c < nc; ++c) {
+        const llep_chunk ch = chunks[(size_t)e * MC + c];
+        if (g >= ch.start && g < ch.end) {
+          dev = ch.device;
+          row = a.chunk_row[(size_t)e * MC + c] + (g - ch.start);
+          break;
+        }
+      }
+    }
+    a.slot_dst[2 * j] = dev;
+    a.slot_dst[2 * j + 1] = row;
+    if (dev >= 0) a.peer_g[dev][row] = a.w[j];
+  }
+  const int nv = a.D / 8;  // 16-byte vectors per row
+  const int4 *src = reinterpret_cast<const int4 *>(a.x) + t * nv;
+  for (int i0 = 0; i0 < nv; i0 += 32 * 4) {
+    int4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * 32 + lane;
+      if (i < nv) v[u] = __ldg(src + i);
+    }
+    for (int k = 0; k < K; ++k) {
+      const int d = __shfl_sync(0xffffffffu, dev, k);
+      const int r = __shfl_sync(0xffffffffu, row, k);
+      if (d < 0) continue;
+      int4 *dst = reinterpret_cast<int4 *>(a.peer_x[d]) + (int64_t)r * nv;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * 32 + lane;
+        if (i < nv) dst[i] = v[u];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ a10: combine
+// One warp per token: out[t] = Σ_{k=0..K-1} Y[dst(t,k)] in slot order, fp32 accumulation,
+// one bf16 rounding (reverse All-to-All + reverse sort + sum over K).
+constexpr int kCombineWarps = 8;
+constexpr int kCombineKMax = 8;
+
+__device__ __forceinline__ void acc_bf16x8(float *acc, const int4 &v) {
+  const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    acc[2 * i] += f.x;
+    acc[2 * i + 1] += f.y;
+  }
+}
+
+__global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * kCombineWarps + (threadIdx.x >> 5);
+  if (t >= a.B) return;
+  const int K = a.K;
+  int dev = -1, row = 0;
+  if (lane < K) {
+    dev = a.slot_dst[2 * (t * K + lane)];
+    row = a.slot_dst[2 * (t * K + lane) + 1];
+  }
+  const int nv = a.D / 8;
+  int4 *dst = reinterpret_cast<int4 *>(a.out) + t * nv;
+  for (int i = lane; i < nv; i += 32) {
+    float acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.f;
+    for (int k0 = 0; k0 < K; k0 += kCombineKMax) {
+      int4 v[kCombineKMax];
+#pragma unroll
+      for (int kk = 0; kk < kCombineKMax; ++kk) {
+        const int k = k0 + kk;
+        const int d = __shfl_sync(0xffffffffu, dev, k & 31);
+        const int r = __shfl_sync(0xffffffffu, row, k & 31);
+        v[kk] = make_int4(0, 0, 0, 0);
+        if (k < K && d >= 0)
+          v[kk] = *(reinterpret_cast<const int4 *>(a.peer_y[d]) + (int64_t)r * nv + i);
+      }
+#pragma unroll
+      for (int kk = 0; kk < kCombineKMax; ++kk)
+        if (k0 + kk < K) acc_bf16x8(acc, v[kk]);
+    }
+    int4 o;
+    __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(acc[2 * u], acc[2 * u + 1]);
+    dst[i] = o;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_tile_count(const int32_t *ids, int64_t n_slots, int32_t N, int32_t *tile_cnt,
+                              int32_t *err, cudaStream_t s) {
+  const int n_tiles = (int)((n_slots + kTileSlots - 1) / kTileSlots);
+  if (n_tiles == 0) return cudaSuccess;
+  tile_count_kernel<<<n_tiles, kCountThreads, sizeof(int32_t) * N, s>>>(ids, n_slots, N, tile_cnt, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_scan(const int32_t *tile_cnt, int32_t n_tiles, int32_t N, int32_t *tile_off,
+                             int32_t *cnt, cudaStream_t s) {
+  tile_scan_kernel<<<(N + 127) / 128, 128, 0, s>>>(tile_cnt, n_tiles, N, tile_off, cnt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_local_rank(const int32_t *ids, int64_t n_slots, int32_t N, const int32_t *tile_off,
+                              int32_t *local_rank, cudaStream_t s) {
+  const int n_tiles = (int)((n_slots + kTileSlots - 1) / kTileSlots);
+  if (n_tiles == 0) return cudaSuccess;
+  const size_t smem = sizeof(int32_t) * kRankWarps * N;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(local_rank_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  local_rank_kernel<<<n_tiles, kRankThreads, smem, s>>>(ids, n_slots, N, tile_off, local_rank);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_push_counts(const int32_t *cnt, int32_t N, int32_t rank, int32_t P,
+                               int32_t *const *peer_lm, cudaStream_t s) {
+  push_counts_kernel<<<P, 256, 0, s>>>(cnt, N, rank, P, peer_lm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_barrier(uint32_t *const *peer_flags, int32_t rank, int32_t P, uint32_t epoch,
+                           int32_t *err, cudaStream_t s) {
+  barrier_kernel<<<1, 32, 0, s>>>(peer_flags, rank, P, epoch, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dispatch(const DispatchArgs &a, cudaStream_t s) {
+  if (a.B == 0) return cudaSuccess;
+  const int64_t blocks = (a.B + kDispatchWarps - 1) / kDispatchWarps;
+  dispatch_kernel<<<(unsigned)blocks, kDispatchWarps * 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const CombineArgs &a, cudaStream_t s) {
+  if (a.B == 0) return cudaSuccess;
+  const int64_t blocks = (a.B + kCombineWarps - 1) / kCombineWarps;
+  combine_kernel<<<(unsigned)blocks, kCombineWarps * 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace llep

@@ -1,0 +1,269 @@
+"""Thin ctypes binding of the C-ABI library `libllep.so` (include/llep.h).
+
+Argument marshalling only: every step of the layer runs in the library's CUDA kernels.  torch is
+used for device memory, streams and (for P > 1) the process group that carries the 64-byte IPC
+handles of the symmetric arenas.  There is no CPU fallback: if the library is missing, importing
+this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import struct
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libllep.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2601_17111_b200.build`")
+_lib = ctypes.CDLL(LIB_PATH)
+
+STATUS = {0: "OK", 1: "INVALID", 2: "PLAN", 3: "ROUTING", 4: "NOMEM", 5: "CUDA", 6: "COMM"}
+
+
+class LLEPError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"LLEP_ERR_{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_double), ("min_chunk", ctypes.c_int64), ("lambda_", ctypes.c_double)]
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("n_experts", ctypes.c_int32), ("top_k", ctypes.c_int32), ("d_model", ctypes.c_int32),
+                ("d_ff", ctypes.c_int32), ("world_size", ctypes.c_int32)]
+
+
+class Requirements(ctypes.Structure):
+    _fields_ = [("rows_needed", ctypes.c_int64), ("foreign_needed", ctypes.c_int32), ("fits", ctypes.c_int32),
+                ("my_rows", ctypes.c_int64), ("my_groups", ctypes.c_int32), ("fallback_ep", ctypes.c_int32),
+                ("force_count", ctypes.c_int32), ("n_transfers", ctypes.c_int32)]
+
+
+_vp, _i32, _i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+_SIGS = {
+    "llep_last_error": (ctypes.c_char_p, []),
+    "llep_version": (ctypes.c_char_p, []),
+    "llep_plan_bytes": (ctypes.c_size_t, [_i32, _i32]),
+    "llep_plan": (ctypes.c_int, [_vp, _i32, _i32, ctypes.POINTER(Params), _vp]),
+    "llep_plan_ep": (ctypes.c_int, [_vp, _i32, _i32, ctypes.POINTER(Params), _vp]),
+    "llep_plan_device": (ctypes.c_int, [_vp, _i32, _i32, ctypes.POINTER(Params), _i32, _vp, _vp]),
+    "llep_context_create": (ctypes.c_int, [ctypes.POINTER(Shape), _i32, _i32, _i64, ctypes.POINTER(_vp)]),
+    "llep_context_destroy": (None, [_vp]),
+    "llep_context_ipc_handle": (ctypes.c_int, [_vp, _vp]),
+    "llep_context_open_peers": (ctypes.c_int, [_vp, _vp, _i32]),
+    "llep_context_reserve": (ctypes.c_int, [_vp, _i64, _i32]),
+    "llep_context_device_bytes": (_i64, [_vp]),
+    "llep_prepare": (ctypes.c_int, [_vp, _vp, _i64, ctypes.POINTER(Params), _i32, _vp,
+                                    ctypes.POINTER(Requirements), _vp]),
+    "llep_moe_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "llep_debug_copy": (ctypes.c_int, [_vp, _i32, _vp, _i64, _vp]),
+    "llep_grouped_gemm": (ctypes.c_int, [_i32, _vp, _i64, _i32, _vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
+}
+EXPORTS = tuple(_SIGS)
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+DBG_LOAD_MATRIX, DBG_SLOT_DST, DBG_GROUPS, DBG_RECV_X, DBG_ACT, DBG_Y, DBG_LOCAL_RANK, DBG_RECV_G = range(1, 9)
+
+
+def _check(code: int) -> None:
+    if code != 0:
+        raise LLEPError(code, _lib.llep_last_error().decode())
+
+
+def version() -> str:
+    return _lib.llep_version().decode()
+
+
+def params(alpha: float = 1.0, min_chunk: int = 1024, lam: float = 1.3) -> Params:
+    return Params(float(alpha), int(min_chunk), float(lam))
+
+
+# ------------------------------------------------------------------------------ plans
+HEADER = struct.Struct("<iiiiii q q q iiii")
+
+
+@dataclass
+class Plan:
+    n_experts: int
+    world: int
+    fallback: bool
+    force_count: int
+    n_transfers: int
+    total: int
+    capacity: int
+    max_assigned: int
+    assigned: List[int]
+    chunks: List[List[Tuple[int, int, int]]]
+    transfers: List[Tuple[int, int, int]]
+    raw: bytes
+
+
+def plan_bytes(n_experts: int, world: int) -> int:
+    return int(_lib.llep_plan_bytes(n_experts, world))
+
+
+def parse_plan(blob: bytes) -> Plan:
+    (N, P, MC, fb, forces, ntr, S, cap, mx, oa, on, oc, orr) = HEADER.unpack_from(blob, 0)
+    assigned = list(np.frombuffer(blob, dtype=np.int64, count=P, offset=oa))
+    nch = np.frombuffer(blob, dtype=np.int32, count=N, offset=on)
+    ch = np.frombuffer(blob, dtype=np.int32, count=N * MC * 3, offset=oc).reshape(N, MC, 3)
+    rep = np.frombuffer(blob, dtype=np.uint8, count=N * P, offset=orr).reshape(N, P)
+    chunks = [[tuple(int(v) for v in ch[e, c]) for c in range(int(nch[e]))] for e in range(N)]
+    M = N // P
+    transfers = [(e, e // M, d) for e in range(N) for d in range(P) if rep[e, d]]
+    return Plan(N, P, bool(fb), forces, ntr, S, cap, mx, [int(a) for a in assigned], chunks, transfers,
+                bytes(blob))
+
+
+def plan_host(loads: Sequence[int], world: int, alpha: float = 1.0, min_chunk: int = 1024,
+              lam: float = 1.3, ep: bool = False) -> Plan:
+    """llep_plan / llep_plan_ep on the host."""
+    l = np.ascontiguousarray(np.asarray(loads, dtype=np.int64))
+    N = int(l.size)
+    nb = plan_bytes(N, world)
+    if nb == 0:
+        raise LLEPError(1, "N and P must be >= 1")
+    buf = (ctypes.c_uint8 * nb)()
+    f = _lib.llep_plan_ep if ep else _lib.llep_plan
+    _check(f(l.ctypes.data, N, world, ctypes.byref(params(alpha, min_chunk, lam)), buf))
+    return parse_plan(bytes(buf))
+
+
+def _stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def plan_device(load_matrix, world: int, alpha: float = 1.0, min_chunk: int = 1024, lam: float = 1.3,
+                ep: bool = False, out=None):
+    """llep_plan_device on a [P, N] int32 CUDA tensor -> uint8 CUDA tensor (the plan blob)."""
+    import torch
+    P, N = load_matrix.shape
+    assert P == world and load_matrix.dtype == torch.int32 and load_matrix.is_cuda
+    lm = load_matrix.contiguous()
+    if out is None:
+        out = torch.empty(plan_bytes(N, P), dtype=torch.uint8, device=lm.device)
+    _check(_lib.llep_plan_device(lm.data_ptr(), N, P, ctypes.byref(params(alpha, min_chunk, lam)),
+                                 int(ep), out.data_ptr(), _stream_ptr()))
+    return out
+
+
+# ------------------------------------------------------------------------------ context
+class Context:
+    """One rank's LLEP context: scratch, symmetric arena, peer mappings."""
+
+    def __init__(self, n_experts: int, top_k: int, d_model: int, d_ff: int, world: int, rank: int,
+                 device: int, max_tokens: int, group=None):
+        import torch
+        self.shape = Shape(n_experts, top_k, d_model, d_ff, world)
+        self.N, self.K, self.D, self.H, self.P, self.rank = n_experts, top_k, d_model, d_ff, world, rank
+        self.M = n_experts // world
+        self.device = device
+        self.group = group
+        self.max_tokens = max_tokens
+        h = _vp()
+        torch.cuda.set_device(device)
+        _check(_lib.llep_context_create(ctypes.byref(self.shape), rank, device, max_tokens, ctypes.byref(h)))
+        self._h = h
+        self.last_req: Optional[Requirements] = None
+        if world > 1:
+            self.exchange_handles()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            _lib.llep_context_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- symmetric arena
+    def exchange_handles(self) -> None:
+        import torch.distributed as dist
+        buf = (ctypes.c_uint8 * 64)()
+        _check(_lib.llep_context_ipc_handle(self._h, buf))
+        mine = bytes(buf)
+        allh: list = [None] * self.P
+        dist.all_gather_object(allh, mine, group=self.group)
+        blob = b"".join(allh)
+        _check(_lib.llep_context_open_peers(self._h, blob, self.P))
+
+    def reserve(self, rows: int, foreign: int) -> None:
+        _check(_lib.llep_context_reserve(self._h, int(rows), int(foreign)))
+        if self.P > 1:
+            self.exchange_handles()
+
+    def device_bytes(self) -> int:
+        return int(_lib.llep_context_device_bytes(self._h))
+
+    # -- the hot path
+    def prepare(self, topk_ids, alpha=1.0, min_chunk=1024, lam=1.3, ep=False, plan_out=None):
+        import torch
+        assert topk_ids.dtype == torch.int32 and topk_ids.is_cuda and topk_ids.is_contiguous()
+        if plan_out is None:
+            plan_out = torch.empty(plan_bytes(self.N, self.P), dtype=torch.uint8, device=topk_ids.device)
+        req = Requirements()
+        _check(_lib.llep_prepare(self._h, topk_ids.data_ptr(), topk_ids.shape[0],
+                                 ctypes.byref(params(alpha, min_chunk, lam)), int(ep), plan_out.data_ptr(),
+                                 ctypes.byref(req), _stream_ptr()))
+        if not req.fits:
+            # identical on every rank (replicated plan): grow symmetrically, re-map peers
+            self.reserve(int(req.rows_needed * 1.0), int(req.foreign_needed))
+            req.fits = 1
+        self.last_req = req
+        return plan_out, req
+
+    def forward(self, x, topk_ids, topk_w, w13, w2, plan, out=None):
+        import torch
+        B = x.shape[0]
+        for t, dt in ((x, torch.bfloat16), (topk_ids, torch.int32), (topk_w, torch.float32),
+                      (w13, torch.bfloat16), (w2, torch.bfloat16)):
+            assert t.dtype == dt and t.is_cuda and t.is_contiguous(), (t.dtype, dt)
+        assert w13.shape == (self.M, 2 * self.H, self.D) and w2.shape == (self.M, self.D, self.H)
+        if out is None:
+            out = torch.empty((B, self.D), dtype=torch.bfloat16, device=x.device)
+        _check(_lib.llep_moe_forward(self._h, x.data_ptr(), topk_ids.data_ptr(), topk_w.data_ptr(), B,
+                                     w13.data_ptr(), w2.data_ptr(), plan.data_ptr(), out.data_ptr(),
+                                     _stream_ptr()))
+        return out
+
+    def __call__(self, x, topk_ids, topk_w, w13, w2, alpha=1.0, min_chunk=1024, lam=1.3, ep=False,
+                 plan_out=None, out=None):
+        """One MoE-layer forward (Alg. 4): prepare (histogram, exchange, plan, layout) + forward."""
+        plan, _ = self.prepare(topk_ids, alpha, min_chunk, lam, ep, plan_out)
+        return self.forward(x, topk_ids, topk_w, w13, w2, plan, out)
+
+    def debug(self, what: int, n: int, dtype):
+        import torch
+        t = torch.empty(n, dtype=dtype, device=f"cuda:{self.device}")
+        _check(_lib.llep_debug_copy(self._h, what, t.data_ptr(), n, _stream_ptr()))
+        return t
+
+
+def grouped_gemm(mode: int, a, w, groups: Sequence[Tuple[int, int, int]], nout: int, gate=None, out=None):
+    """llep_grouped_gemm: groups = [(expert, row_base, n_rows)] (host), a [rows, kdim] bf16,
+    mode 0: w [E, 2*nout, kdim] -> SwiGLU [rows, nout]; mode 1: w [E, nout, kdim] -> gate*(a wᵀ)."""
+    import torch
+    rows, kdim = a.shape
+    if out is None:
+        out = torch.zeros((rows, nout), dtype=torch.bfloat16, device=a.device)
+    g = np.asarray([[e, rb, n, 0] for (e, rb, n) in groups], dtype=np.int32).reshape(-1)
+    g = np.ascontiguousarray(g)
+    _check(_lib.llep_grouped_gemm(mode, a.data_ptr(), rows, kdim, w.data_ptr(), w.shape[0], nout,
+                                  g.ctypes.data, len(groups), gate.data_ptr() if gate is not None else None,
+                                  out.data_ptr(), _stream_ptr()))
+    return out

@@ -1,0 +1,96 @@
+"""The C-ABI library loads, exports every symbol llep.h declares, and its HOST planner
+(llep_plan / llep_plan_ep, no GPU needed) is bit-identical to the oracle -- CPU only."""
+import os
+import random
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2601_17111_b200 import build
+    build.build()
+    from paper_2601_17111_b200 import llep
+    return llep
+
+
+def test_exports_match_header(L):
+    hdr = open(os.path.join(ROOT, "include", "llep.h")).read()
+    declared = set(re.findall(r"^(?:const\s+)?[a-z_0-9]+\s*\*?\s*(llep_[a-z_0-9]+)\(", hdr, re.M))
+    assert declared, "no declarations parsed"
+    import ctypes
+    lib = ctypes.CDLL(L.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(L.EXPORTS)
+
+
+def test_plan_bytes_and_header(L):
+    assert L.plan_bytes(128, 8) > 0 and L.plan_bytes(0, 8) == 0
+    p = L.plan_host([10, 0, 0, 0], 2, 1.0, 1, 1.0)
+    assert p.n_experts == 4 and p.world == 2 and p.chunks[0] == [(0, 0, 5), (1, 5, 10)]
+    assert p.assigned == [5, 5] and p.transfers == [(0, 0, 1)] and p.capacity == 5
+
+
+def test_host_plan_errors(L):
+    for args in [([1, 2, 3], 2, 1.0, 0, 1.3), ([1, 2], 2, 0.5, 0, 1.3), ([1, 2], 2, 1.0, 0, 0.9),
+                 ([1, -2], 2, 1.0, 0, 1.3), ([1, 2], 2, 1.0, -1, 1.3)]:
+        with pytest.raises(L.LLEPError) as ei:
+            L.plan_host(*args)
+        assert ei.value.code == 1
+
+
+def _same(p, q):
+    assert [list(A) for A in p.chunks] == [list(A) for A in q.chunks]
+    assert p.assigned == q.assigned and p.capacity == q.capacity and p.total == q.total
+    assert p.fallback == q.fallback and p.force_count == q.force_count
+    assert p.transfers == q.transfers
+
+
+def test_host_plan_matches_oracle_fuzz(L):
+    from oracle import planner as O1
+    rng = random.Random(2024)
+    for i in range(4000):
+        P = rng.choice([1, 2, 3, 4, 8, 16])
+        M = rng.choice([1, 2, 4, 8, 16])
+        N = P * M
+        alpha = rng.choice([1.0, 1.0, 1.5, 2.0, rng.uniform(1, 3)])
+        m = rng.choice([0, 1, 2, 8, 64, 1024])
+        lam = rng.choice([1.0, 1.3, 2.0])
+        kind = rng.randrange(3)
+        if kind == 0:
+            l = [rng.randint(0, 60) for _ in range(N)]
+        elif kind == 1:
+            l = [rng.randint(0, 20) for _ in range(N)]
+            for _ in range(rng.randint(1, 3)):
+                l[rng.randrange(N)] += rng.randint(100, 20000)
+        else:
+            l = [rng.choice([0, 1, 5, 3000]) for _ in range(N)]
+        _same(L.plan_host(l, P, alpha, m, lam), O1.plan(l, P, alpha, m, lam))
+        _same(L.plan_host(l, P, alpha, m, lam, ep=True), O1.ep_plan(l, P, alpha, fallback=False))
+
+
+def test_host_plan_golden_and_paper_configs(L, golden_dir):
+    import json
+    from oracle import planner as O1
+    from synth import workload as W
+    g = json.load(open(os.path.join(golden_dir, "planner_traces.json")))
+    for c in g["cases"]:
+        p = L.plan_host(c["loads"], c["world"], c["alpha"], c["min_chunk"], 1.0)
+        assert [[list(x) for x in A] for A in p.chunks] == c["chunks"]
+        assert p.force_count == c["force_count"]
+    for name in ("tiny", "g20", "g120", "q3"):
+        sh = W.CONFIGS[name]
+        for pct, y in [(None, 0), (30, 1), (50, 4), (80, 16), (95, 1)]:
+            if y > sh.n_experts:
+                continue
+            cnt = W.slot_counts(sh.n_experts, sh.tokens_per_rank * sh.top_k, pct, y)
+            for P in (1, 2, 4, 8):
+                if sh.n_experts % P:
+                    continue
+                l = (cnt * P).tolist()
+                _same(L.plan_host(l, P), O1.plan(l, P))

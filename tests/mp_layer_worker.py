@@ -1,0 +1,49 @@
+"""Spawn P ranks (processes) that share one GPU and run the LLEP and EP layer through the C ABI.
+
+    python mp_layer_worker.py P CFG HOT_PCT N_HOT OUTDIR
+
+The ranks bootstrap a gloo process group on 127.0.0.1 (plumbing only: it carries the 64-byte CUDA
+IPC handles); all data moves through the library's peer-mapped arenas and device barriers.
+Each rank writes OUTDIR/rank{p}.npz with its LLEP output, EP output and plan blob."""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, HERE)
+
+
+def worker(rank, P, cfg, pct, nhot, outdir):
+    import torch
+    import torch.distributed as dist
+    import layer_case as LC
+    from synth import workload as W
+    from paper_2601_17111_b200 import llep as L
+
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    dev = int(os.environ.get("LLEP_TEST_DEVICE", "0"))
+    torch.cuda.set_device(dev)
+    sh0 = W.CONFIGS[cfg]
+    sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, P)
+    x, ids, gates, w13, w2, _, _ = LC.rank_inputs(sh, rank, pct, nhot, 21, f"cuda:{dev}")
+    ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, P, rank, dev, sh.tokens_per_rank)
+    out_llep = ctx(x, ids, gates, w13, w2)
+    plan = ctx.prepare(ids)[0]          # plan of the LLEP call (deterministic)
+    plan_np = plan.cpu().numpy()
+    out_llep2 = ctx.forward(x, ids, gates, w13, w2, plan)   # second iteration on the same arena
+    out_ep = ctx(x, ids, gates, w13, w2, ep=True)
+    torch.cuda.synchronize()
+    assert torch.equal(out_llep, out_llep2), "iteration-to-iteration mismatch"
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), llep=out_llep.float().cpu().numpy(),
+             ep=out_ep.float().cpu().numpy(), plan=plan_np)
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    import torch.multiprocessing as mp
+    P, cfg, pct, nhot, outdir = int(sys.argv[1]), sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), sys.argv[5]
+    mp.spawn(worker, args=(P, cfg, pct, nhot, outdir), nprocs=P, join=True)

@@ -1,0 +1,105 @@
+"""GPU kernel tests through the C ABI: device planner (bit-exact) and the tcgen05 grouped GEMMs."""
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2601_17111_b200 import llep
+    return llep
+
+
+def _same_plan(p, q):
+    assert [list(A) for A in p.chunks] == [list(A) for A in q.chunks]
+    assert p.assigned == q.assigned and p.capacity == q.capacity and p.total == q.total
+    assert p.fallback == q.fallback and p.force_count == q.force_count
+    assert p.transfers == q.transfers
+
+
+def test_device_planner_bit_exact(L):
+    """Device plan blob == host plan blob byte for byte, and == the oracle (O1) field by field."""
+    from oracle import planner as O1
+    rng = random.Random(77)
+    dev = torch.device("cuda:0")
+    for i in range(600):
+        P = rng.choice([1, 2, 3, 4, 8, 16, 32])
+        M = rng.choice([1, 2, 4, 8, 16])
+        N = P * M
+        if N > 1024:
+            continue
+        alpha = rng.choice([1.0, 1.0, 1.5, 2.0, rng.uniform(1, 3)])
+        m = rng.choice([0, 1, 8, 64, 1024])
+        lam = rng.choice([1.0, 1.3, 2.0])
+        C = np.zeros((P, N), dtype=np.int32)
+        for p in range(P):
+            C[p] = [rng.randint(0, 30) for _ in range(N)]
+            if rng.random() < 0.7:
+                C[p, rng.randrange(N)] += rng.randint(100, 20000)
+        l = C.sum(0).astype(np.int64)
+        for ep in (False, True):
+            blob = L.plan_device(torch.from_numpy(C).to(dev), P, alpha, m, lam, ep=ep)
+            dp = L.parse_plan(blob.cpu().numpy().tobytes())
+            hp = L.plan_host(l, P, alpha, m, lam, ep=ep)
+            assert dp.raw == hp.raw, (i, P, N, alpha, m, lam, ep)
+            ref = O1.ep_plan(l, P, alpha, fallback=False) if ep else O1.plan(l.tolist(), P, alpha, m, lam)
+            _same_plan(dp, ref)
+
+
+def _ref_gemm(mode, a, w, groups, nout, gate):
+    out = torch.zeros((a.shape[0], nout), dtype=torch.float32, device=a.device)
+    for (e, rb, n) in groups:
+        x = a[rb:rb + n].float()
+        if mode == 0:
+            g = x @ w[e, :nout].float().T
+            u = x @ w[e, nout:].float().T
+            out[rb:rb + n] = torch.nn.functional.silu(g) * u
+        else:
+            out[rb:rb + n] = gate[rb:rb + n, None] * (x @ w[e].float().T)
+    return out
+
+
+@pytest.mark.parametrize("mode,kdim,nout", [
+    (0, 256, 512),    # TINY GEMM1 (BN=256)
+    (1, 512, 256),    # TINY GEMM2
+    (0, 2880, 2880),  # gpt-oss GEMM1 (BN=240: 120 gate + 120 up)
+    (1, 2880, 2880),  # gpt-oss GEMM2 (BN=240)
+    (0, 2048, 768),   # Qwen3 GEMM1
+    (1, 768, 2048),   # Qwen3 GEMM2
+    (0, 192, 200),    # ragged: masked tail tile, partial K block
+    (1, 200, 136),
+])
+def test_grouped_gemm(L, mode, kdim, nout):
+    g = torch.Generator(device="cuda").manual_seed(kdim * 7 + nout)
+    E = 3
+    sizes = [1, 300, 0, 129, 128, 77]
+    groups, rb = [], 0
+    for i, n in enumerate(sizes):
+        if n == 0:
+            continue
+        groups.append((i % E, rb, n))
+        rb += (n + 127) // 128 * 128
+    rows = rb + 128
+    a = (torch.randn((rows, kdim), generator=g, device="cuda") ).to(torch.bfloat16)
+    wr = 2 * nout if mode == 0 else nout
+    w = (torch.randn((E, wr, kdim), generator=g, device="cuda") / kdim ** 0.5).to(torch.bfloat16)
+    gate = torch.rand((rows,), generator=g, device="cuda") if mode == 1 else None
+    out = L.grouped_gemm(mode, a, w, groups, nout, gate)
+    torch.cuda.synchronize()
+    ref = _ref_gemm(mode, a, w, groups, nout, gate)
+    for (e, rb, n) in groups:
+        y, r = out[rb:rb + n].float(), ref[rb:rb + n]
+        err = (y - r).abs().max().item() / max(r.abs().max().item(), 1e-6)
+        l2 = ((y - r).norm() / r.norm().clamp_min(1e-12)).item()
+        assert err < 2e-2 and l2 < 5e-3, (e, rb, n, err, l2)
+    # rows outside groups are untouched (zeros)
+    mask = torch.ones(rows, dtype=torch.bool, device="cuda")
+    for (e, rb, n) in groups:
+        mask[rb:rb + n] = False
+    assert out[mask].abs().max().item() == 0.0

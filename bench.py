@@ -1,0 +1,422 @@
+"""Benchmark of the LLEP MoE-layer forward (BASELINE.json metric: MoE-layer tokens/s and peak GB/GPU,
+LLEP vs EP on the same kernels, by imbalance).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config g120] [--hot 95 --nhot 1] [--sweep]
+    python bench.py --impl reference ...        # the float64 CPU oracle as the reference arm
+
+One step = one whole layer pass on every rank: histogram + load exchange + planner + layout (llep_prepare)
+and dispatch + weight migration + GEMM1/SwiGLU + GEMM2/gate + combine (llep_moe_forward), through the
+C ABI.  Inputs are resident in HBM before the timed region (value) or copied from pinned host memory
+inside it (e2e).  Weak scaling: each rank holds B tokens of the configuration, P = N GPUs.
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import workload as W  # noqa: E402
+
+METRIC = "MoE-layer tokens/s (LLEP, gpt-oss-120b-shaped layer, 95% of slots into 1 hot expert)"
+SEED = W.BASE_SEED
+
+
+# ------------------------------------------------------------------------------ helpers
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"bf16_tflops": d["bf16_tflops"], "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "hbm_gbs": d["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-i", str(self.device), "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
+    group = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        group = dist.group.WORLD
+    return world, rank, local, group
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    import torch
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def run_mode(L, shape, rank, local, world, group, inputs, ep: bool, steps: int, warmup: int, clocks=None):
+    """Warm up, then time exactly `steps` layer steps with CUDA events (max over ranks)."""
+    import torch
+    x, ids, gates, w13, w2 = inputs
+    torch.cuda.reset_peak_memory_stats()
+    ctx = L.Context(shape.n_experts, shape.top_k, shape.d_model, shape.d_ff, world, rank, local,
+                    shape.tokens_per_rank, group=group)
+    out = torch.empty_like(x)
+    plan_buf = torch.empty(L.plan_bytes(shape.n_experts, world), dtype=torch.uint8, device=x.device)
+    for _ in range(warmup):
+        ctx(x, ids, gates, w13, w2, ep=ep, plan_out=plan_buf, out=out)
+    ctx.set_timing(True)
+    ctx.stats(reset=True)
+    barrier(world)
+    if clocks:
+        clocks.start()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        ctx(x, ids, gates, w13, w2, ep=ep, plan_out=plan_buf, out=out)
+    e1.record(s)
+    barrier(world)
+    clk = clocks.stop() if clocks else None
+    ms = e0.elapsed_time(e1)
+    st = ctx.stats(reset=True)
+    ctx.set_timing(False)
+    req = ctx.last_req
+    peak = torch.cuda.max_memory_allocated() + ctx.device_bytes()
+    res = {
+        "ms_total": max_over_ranks(ms, world),
+        "ms_per_step": max_over_ranks(ms, world) / steps,
+        "stats": st,
+        "peak_bytes": max_over_ranks(float(peak), world),
+        "my_rows": int(req.my_rows), "n_transfers": int(req.n_transfers), "fallback": int(req.fallback_ep),
+        "force_count": int(req.force_count), "clocks": clk, "out": out, "ctx": ctx,
+    }
+    return res
+
+
+def run_e2e(L, ctx, shape, host, dev, steps, warmup, world, ep=False):
+    """Public API end to end: pinned host inputs -> H2D -> layer -> D2H of the output, every step."""
+    import torch
+    x_h, ids_h, g_h = host
+    x, ids, gates, w13, w2 = dev
+    out = torch.empty_like(x)
+    out_h = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+    plan_buf = torch.empty(L.plan_bytes(shape.n_experts, world), dtype=torch.uint8, device=x.device)
+
+    def step():
+        x.copy_(x_h, non_blocking=True)
+        ids.copy_(ids_h, non_blocking=True)
+        gates.copy_(g_h, non_blocking=True)
+        ctx(x, ids, gates, w13, w2, ep=ep, plan_out=plan_buf, out=out)
+        out_h.copy_(out, non_blocking=True)
+
+    for _ in range(warmup):
+        step()
+    barrier(world)
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        step()
+    e1.record(s)
+    barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    h2d = x_h.numel() * 2 + ids_h.numel() * 4 + g_h.numel() * 4
+    d2h = out_h.numel() * 2
+    return ms / steps, h2d, d2h
+
+
+def cpu_baseline(shape, hot, nhot, budget_s=12.0, max_tokens=8192):
+    """The float64 oracle (O3), as it stands, on this host's cores for a bounded sample of rank 0's
+    tokens: tokens whose K experts all lie in {0..7} (the hot expert + 7 cold ones; per-slot work is
+    6*D*H FLOPs for every expert, so throughput per token is representative)."""
+    from oracle import layer as O3
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    ids = W.routing_ids(shape, 0, hot, nhot, SEED)
+    gates = W.gate_weights(shape.tokens_per_rank, shape.top_k, 0, SEED).astype(np.float64)
+    keep = np.nonzero((ids < 8).all(axis=1))[0]
+    cache = {}
+
+    def weights(e):
+        if e not in cache:
+            wg, wu, wd = W.expert_weights_bits(int(e), shape.d_model, shape.d_ff, SEED)
+            cache[e] = (W.bf16_bits_to_f64(wg), W.bf16_bits_to_f64(wu), W.bf16_bits_to_f64(wd))
+        return cache[e]
+
+    for e in np.unique(ids[keep[:max_tokens]]):
+        weights(int(e))
+    xb = W.tokens_bits(shape.tokens_per_rank, shape.d_model, 0, SEED)
+    x = W.bf16_bits_to_f64(xb)
+    done, t_total, chunk = 0, 0.0, 256
+    O3.moe_forward(x[keep[:16]], ids[keep[:16]], gates[keep[:16]], weights)  # BLAS warm-up
+    while done < min(max_tokens, keep.size) and t_total < budget_s:
+        sel = keep[done:done + chunk]
+        t0 = time.perf_counter()
+        O3.moe_forward(x[sel], ids[sel], gates[sel], weights)
+        t_total += time.perf_counter() - t0
+        done += sel.size
+    return {"value": done / t_total, "unit": "tokens/s", "cores": int(threads), "kind": "oracle",
+            "host_cpus": len(os.sched_getaffinity(0)),
+            "sample": f"{done} tokens of rank 0 (all K={shape.top_k} slots in experts 0..7) of the "
+                      f"{W.scenario_name(hot, nhot)} workload, float64 O3 (numpy BLAS), {t_total:.1f} s"}
+
+
+def gpu_main(args):
+    import torch
+    world, rank, local, group = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    from paper_2601_17111_b200 import llep as L
+    base = W.CONFIGS[args.config]
+    shape = W.LayerShape(base.n_experts, base.top_k, base.d_model, base.d_ff, base.tokens_per_rank, world)
+    B, K, D, H, M = shape.tokens_per_rank, shape.top_k, shape.d_model, shape.d_ff, shape.experts_per_rank
+    dev = torch.device(f"cuda:{local}")
+    hot = None if args.hot == 0 else args.hot
+    ids_np = W.routing_ids(shape, rank, hot, args.nhot, SEED)
+    g_np = W.gate_weights(B, K, rank, SEED)
+    x = W.tokens_torch(B, D, rank, dev, SEED)
+    ids = torch.from_numpy(ids_np).to(dev)
+    gates = torch.from_numpy(g_np).to(dev)
+    w13, w2 = W.expert_weights_torch(range(rank * M, (rank + 1) * M), D, H, dev, SEED)
+    inputs = (x, ids, gates, w13, w2)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local) if rank == 0 else None
+    ll = run_mode(L, shape, rank, local, world, group, inputs, False, args.steps, args.warmup, clocks)
+    ll_ctx = ll.pop("ctx")
+    ep = run_mode(L, shape, rank, local, world, group, inputs, True, args.steps, args.warmup)
+    ep.pop("ctx").close()
+    same = bool(torch.equal(ll.pop("out"), ep.pop("out")))
+    e2e = None
+    if not args.no_e2e:
+        host = (x.cpu().pin_memory(), ids.cpu().pin_memory(), gates.cpu().pin_memory())
+        dev_bufs = (torch.empty_like(x), torch.empty_like(ids), torch.empty_like(gates), w13, w2)
+        ms_e2e, h2d, d2h = run_e2e(L, ll_ctx, shape, host, dev_bufs, max(3, args.steps // 2), 2, world)
+        e2e = {"value": world * B / (ms_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e}
+    ll_ctx.close()
+
+    sweep = []
+    if args.sweep:
+        for (h, y) in [(None, 0), (30, 1), (50, 1), (80, 1), (95, 4), (95, 16)]:
+            ids2 = torch.from_numpy(W.routing_ids(shape, rank, h, y, SEED)).to(dev)
+            inp = (x, ids2, gates, w13, w2)
+            a = run_mode(L, shape, rank, local, world, group, inp, False, max(3, args.steps // 2), 2)
+            b = run_mode(L, shape, rank, local, world, group, inp, True, max(3, args.steps // 2), 2)
+            a.pop("ctx").close(); b.pop("ctx").close()
+            sweep.append({"scenario": W.scenario_name(h, y),
+                          "llep_tokens_s": world * B / (a["ms_per_step"] / 1e3),
+                          "ep_tokens_s": world * B / (b["ms_per_step"] / 1e3),
+                          "speedup": b["ms_per_step"] / a["ms_per_step"],
+                          "llep_peak_gb": a["peak_bytes"] / 1e9, "ep_peak_gb": b["peak_bytes"] / 1e9})
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    peaks = load_peaks()
+    st = ll["stats"]
+    calls = max(st["calls"], 1)
+    rows_per_launch = st["gemm_rows"] / calls
+    g1_ms = st["ms"]["gemm1"] / calls
+    g2_ms = st["ms"]["gemm2"] / calls
+    g1_flops = 4.0 * D * H * rows_per_launch
+    g2_flops = 2.0 * D * H * rows_per_launch
+    achieved = g1_flops / (g1_ms / 1e3) / 1e12 if g1_ms > 0 else 0.0
+    peak = peaks["bf16_tflops_sustained"]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(args.config, {}).get("gemm1_dram_bytes_per_launch")
+    step_ms = ll["ms_per_step"]
+    value = world * B / (step_ms / 1e3)
+    line = {
+        "metric": METRIC if args.config == "g120" and args.hot == 95 and args.nhot == 1 else
+        f"MoE-layer tokens/s (LLEP, {args.config}, {W.scenario_name(hot, args.nhot)})",
+        "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded counter-based generator; random-init expert weights)",
+        "config": {"workload": f"{args.config}: N={shape.n_experts} experts, top-{K}, d_model={D}, d_ff={H}, "
+                               f"{B} tokens/rank, P={world}, {W.scenario_name(hot, args.nhot)}; "
+                               f"lambda=1.3 alpha=1 m=1024",
+                   "tokens_per_rank": B, "ep_world": world, "scenario": W.scenario_name(hot, args.nhot),
+                   "l2": f"inputs larger than L2 (x {B * D * 2 / 1e6:.0f} MB/rank, expert weights "
+                         f"{M * 6 * D * H / 1e9:.1f} GB/rank); no flush"},
+        "peak_gb_per_gpu": ll["peak_bytes"] / 1e9,
+        "ep": {"value": world * B / (ep["ms_per_step"] / 1e3), "ms_per_step": ep["ms_per_step"],
+               "peak_gb_per_gpu": ep["peak_bytes"] / 1e9, "my_rows_rank0": ep["my_rows"]},
+        "speedup_vs_ep": ep["ms_per_step"] / step_ms,
+        "llep_equals_ep_bitwise": same,
+        "plan": {"fallback_ep": ll["fallback"], "n_transfers": ll["n_transfers"], "force_count": ll["force_count"],
+                 "rows_rank0": ll["my_rows"]},
+        "phases_ms_per_step": {k: v / calls for k, v in st["ms"].items()},
+        "roofline": {"kernel": "grouped GEMM1 + SwiGLU (tcgen05)", "bound": "tensor", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_kind": f"bf16 dense, sustained, {peaks['source']}",
+                     "flops_per_launch": g1_flops, "ms_per_launch": g1_ms,
+                     "gemm2_tflops": g2_flops / (g2_ms / 1e3) / 1e12 if g2_ms > 0 else 0.0,
+                     "layer_tflops": (g1_flops + g2_flops) / (step_ms / 1e3) / 1e12},
+        "gpu_launches": st["kernel_launches"],
+        "clocks": ll["clocks"],
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if sweep:
+        line["sweep"] = sweep
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(shape, hot, args.nhot)
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ reference arm
+def reference_main(args):
+    """The float64 oracle as the reference arm (tier framing): each step = a bounded sample of the
+    same workload on the host cores; rank 0 only."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    from oracle import layer as O3
+    base = W.CONFIGS[args.config]
+    world = args.gpus
+    shape = W.LayerShape(base.n_experts, base.top_k, base.d_model, base.d_ff, base.tokens_per_rank, world)
+    hot = None if args.hot == 0 else args.hot
+    ids = W.routing_ids(shape, 0, hot, args.nhot, SEED)
+    gates = W.gate_weights(shape.tokens_per_rank, shape.top_k, 0, SEED).astype(np.float64)
+    keep = np.nonzero((ids < 8).all(axis=1))[0]
+    per_step = 64
+    need = keep[: per_step * (args.steps + args.warmup)]
+    cache = {}
+
+    def weights(e):
+        if e not in cache:
+            wg, wu, wd = W.expert_weights_bits(int(e), shape.d_model, shape.d_ff, SEED)
+            cache[e] = (W.bf16_bits_to_f64(wg), W.bf16_bits_to_f64(wu), W.bf16_bits_to_f64(wd))
+        return cache[e]
+
+    for e in np.unique(ids[need]):
+        weights(int(e))
+    x = W.bf16_bits_to_f64(W.token_rows_bits(need, shape.d_model, 0, SEED))
+    for s in range(args.warmup):
+        sl = slice(s * per_step, (s + 1) * per_step)
+        O3.moe_forward(x[sl], ids[need[sl]], gates[need[sl]], weights)
+    t0 = time.perf_counter()
+    for s in range(args.warmup, args.warmup + args.steps):
+        sl = slice(s * per_step, (s + 1) * per_step)
+        O3.moe_forward(x[sl], ids[need[sl]], gates[need[sl]], weights)
+    dt = time.perf_counter() - t0
+    value = args.steps * per_step / dt
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    sample = (f"{per_step} tokens of rank 0 per step (all slots in experts 0..7) of the "
+              f"{W.scenario_name(hot, args.nhot)} workload, float64 O3")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"{args.config} (oracle sample)", "ep_world": world},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": int(threads), "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="llep", choices=["llep", "reference"])
+    ap.add_argument("--config", default="g120", choices=sorted(W.CONFIGS))
+    ap.add_argument("--hot", type=int, default=95, help="percent of slots into the hot experts (0 = balanced)")
+    ap.add_argument("--nhot", type=int, default=1)
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        reference_main(args)
+    else:
+        gpu_main(args)
+
+
+if __name__ == "__main__":
+    main()

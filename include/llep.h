@@ -192,6 +192,36 @@ llep_status llep_moe_forward(llep_context *ctx, const uint16_t *x, const int32_t
                              const float *topk_w, int64_t n_tokens, const uint16_t *w13,
                              const uint16_t *w2, const void *plan, uint16_t *out, void *stream);
 
+/* ------------------------------------------------------------------ measurement
+ * Per-phase device time, from CUDA events recorded on the caller's stream at the phase
+ * boundaries of llep_prepare / llep_moe_forward, accumulated over calls while timing is on:
+ *   ROUTE    a1 + a3 (histogram, scan, stable local ranks)
+ *   EXCHANGE a2 (count push + device barrier + local copy of C)
+ *   PLAN     a4 + a5 (planner kernel + layout kernel)
+ *   DISPATCH a6 + a7 (dispatch kernel, weight pushes joined, device barrier)
+ *   GEMM1    a8 (grouped GEMM + SwiGLU)      GEMM2  a9 (grouped GEMM + gate)
+ *   COMBINE  a10 (device barrier + combine kernel)
+ * kernel_launches counts every kernel the library launched (timing on or off). */
+enum {
+  LLEP_PH_ROUTE = 0,
+  LLEP_PH_EXCHANGE = 1,
+  LLEP_PH_PLAN = 2,
+  LLEP_PH_DISPATCH = 3,
+  LLEP_PH_GEMM1 = 4,
+  LLEP_PH_GEMM2 = 5,
+  LLEP_PH_COMBINE = 6,
+  LLEP_NUM_PHASES = 7
+};
+typedef struct {
+  double ms[LLEP_NUM_PHASES];
+  int64_t calls;            /* completed prepare+forward pairs timed */
+  int64_t kernel_launches;  /* kernels launched since the last reset */
+  int64_t gemm_rows;        /* Σ over timed calls of real rows this rank's GEMMs processed */
+} llep_stats;
+llep_status llep_context_set_timing(llep_context *ctx, int32_t enable);
+/* Synchronises the pending events, writes the totals, resets them if `reset`. */
+llep_status llep_context_stats(llep_context *ctx, llep_stats *out, int32_t reset);
+
 /* ------------------------------------------------------------------ inspection (tests)
  * Copy the last prepare/forward intermediates to caller DEVICE buffers (sizes in elements):
  *   LLEP_DBG_LOAD_MATRIX  int32 [P*N]        LLEP_DBG_SLOT_DST  int32 [2*B*K] (device,row)

@@ -209,7 +209,31 @@ struct llep_context {
   int64_t prepared_tokens = -1;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // measurement
+  bool timing = false, pending = false;
+  cudaEvent_t mark[9] = {};
+  double phase_ms[LLEP_NUM_PHASES] = {};
+  int64_t calls = 0, launches = 0, gemm_rows = 0, pending_rows = 0;
 };
+
+static void mark(llep_context *c, int i, cudaStream_t s) {
+  if (c->timing) cudaEventRecord(c->mark[i], s);
+}
+
+// fold the events of the last completed prepare+forward into the totals
+static void collect(llep_context *c) {
+  if (!c->pending) return;
+  cudaEventSynchronize(c->mark[8]);
+  static const int from[LLEP_NUM_PHASES] = {0, 1, 2, 4, 5, 6, 7};
+  for (int p = 0; p < LLEP_NUM_PHASES; ++p) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->mark[from[p]], c->mark[from[p] + 1]);
+    c->phase_ms[p] += ms;
+  }
+  c->calls += 1;
+  c->gemm_rows += c->pending_rows;
+  c->pending = false;
+}
 
 static void layout_offsets(llep_context *c, int64_t rows, int32_t foreign) {
   size_t off = 0;
@@ -378,6 +402,7 @@ llep_status llep_context_create(const llep_shape *s, int32_t rank, int32_t devic
   if (!e) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
   if (!e) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   if (!e) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  for (int i = 0; i < 9 && !e; ++i) e = cudaEventCreate(&c->mark[i]);
   if (e) {
     llep_context_destroy(c);
     return cuda_status(e, "llep_context_create");
@@ -407,6 +432,8 @@ void llep_context_destroy(llep_context *c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  for (int i = 0; i < 9; ++i)
+    if (c->mark[i]) cudaEventDestroy(c->mark[i]);
   delete c;
 }
 
@@ -465,6 +492,7 @@ static float *const *peer_g(llep_context *c) { return reinterpret_cast<float *co
 static llep_status barrier(llep_context *c, cudaStream_t s) {
   if (c->P == 1) return LLEP_OK;
   ++c->epoch;
+  ++c->launches;
   LLEP_CUDA(launch_barrier(peer_flags(c), c->rank, c->P, c->epoch, c->err + 1, s));
   return LLEP_OK;
 }
@@ -497,6 +525,7 @@ static llep_status run_layout(llep_context *c, const void *plan, cudaStream_t s)
   la.dev_foreign = c->dev_foreign;
   la.summary = c->summary;
   LLEP_CUDA(launch_layout(la, s));
+  ++c->launches;
   return LLEP_OK;
 }
 
@@ -536,26 +565,35 @@ llep_status llep_prepare(llep_context *c, const int32_t *ids, int64_t B, const l
     return LLEP_ERR_COMM;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  collect(c);
+  c->pending = false;
   const int N = c->N, P = c->P;
   const int64_t slots = B * c->K;
   const int n_tiles = (int)((slots + kTileSlots - 1) / kTileSlots);
+  mark(c, 0, s);
   // a1: per-tile histogram + scan -> counts row; a3: stable local ranks
   LLEP_CUDA(launch_tile_count(ids, slots, N, c->tile_cnt, c->err, s));
   if (n_tiles > 0) {
     LLEP_CUDA(launch_tile_scan(c->tile_cnt, n_tiles, N, c->tile_off, c->cnt, s));
+    c->launches += 3;
   } else {
     LLEP_CUDA(cudaMemsetAsync(c->cnt, 0, sizeof(int32_t) * N, s));
   }
   LLEP_CUDA(launch_local_rank(ids, slots, N, c->tile_off, c->local_rank, s));
+  mark(c, 1, s);
   // a2: push the counts row into every rank's load matrix, barrier, keep a local copy
   LLEP_CUDA(launch_push_counts(c->cnt, N, c->rank, P, peer_lm(c), s));
+  ++c->launches;
   if ((st = barrier(c, s)) != LLEP_OK) return st;
   LLEP_CUDA(cudaMemcpyAsync(c->lm_local, c->arena + c->off_lm, sizeof(int32_t) * P * N,
                             cudaMemcpyDeviceToDevice, s));
+  mark(c, 2, s);
   // a4: planner; a5: layout
   LLEP_CUDA(launch_planner(c->lm_local, N, P, prm->alpha, prm->min_chunk, prm->lambda, force_ep,
                            plan_out, s));
+  ++c->launches;
   if ((st = run_layout(c, plan_out, s)) != LLEP_OK) return st;
+  mark(c, 3, s);
   if ((st = read_back(c, plan_out, s)) != LLEP_OK) return st;
   c->prepared_tokens = B;
   if (req) fill_req(c, req);
@@ -610,6 +648,7 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
       ++f;
     }
   }
+  mark(c, 4, s);
   if (any_copy) LLEP_CUDA(cudaEventRecord(c->ev_join, c->side));
   // a6: dispatch (gather-on-send into every destination's receive rows)
   DispatchArgs da;
@@ -630,8 +669,10 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   da.peer_g = peer_g(c);
   da.slot_dst = c->slot_dst;
   LLEP_CUDA(launch_dispatch(da, s));
+  c->launches += B > 0;
   if (any_copy) LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
   if ((st = barrier(c, s)) != LLEP_OK) return st;
+  mark(c, 5, s);
   // a8: GEMM1 + SwiGLU   X [rows, D] -> A [rows, H]
   uint16_t *X = reinterpret_cast<uint16_t *>(c->arena + c->off_x);
   GemmArgs g1;
@@ -651,6 +692,8 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   g1.out = c->act;
   g1.num_sms = c->num_sms;
   if (sum.my_groups > 0 && (st = run_grouped_gemm(g1, s)) != LLEP_OK) return st;
+  c->launches += sum.my_groups > 0;
+  mark(c, 6, s);
   // a9: GEMM2 + gate   A [rows, H] -> Y [rows, D]  (Y reuses X's rows: X is dead after GEMM1)
   GemmArgs g2 = g1;
   g2.mode = 1;
@@ -662,6 +705,8 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   g2.gate = reinterpret_cast<const float *>(c->arena + c->off_g);
   g2.out = X;
   if (sum.my_groups > 0 && (st = run_grouped_gemm(g2, s)) != LLEP_OK) return st;
+  c->launches += sum.my_groups > 0;
+  mark(c, 7, s);
   if ((st = barrier(c, s)) != LLEP_OK) return st;
   // a10: combine (pull each slot's Y row from its device, K-sum in slot order)
   CombineArgs ca;
@@ -672,6 +717,33 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   ca.D = D;
   ca.out = out;
   LLEP_CUDA(launch_combine(ca, s));
+  c->launches += B > 0;
+  mark(c, 8, s);
+  if (c->timing) {
+    c->pending = true;
+    c->pending_rows = sum.my_rows;
+  }
+  return LLEP_OK;
+}
+
+llep_status llep_context_set_timing(llep_context *c, int32_t enable) {
+  if (!c) return invalid("null context");
+  collect(c);
+  c->timing = enable != 0;
+  return LLEP_OK;
+}
+
+llep_status llep_context_stats(llep_context *c, llep_stats *out, int32_t reset) {
+  if (!c || !out) return invalid("null pointer");
+  collect(c);
+  for (int p = 0; p < LLEP_NUM_PHASES; ++p) out->ms[p] = c->phase_ms[p];
+  out->calls = c->calls;
+  out->kernel_launches = c->launches;
+  out->gemm_rows = c->gemm_rows;
+  if (reset) {
+    for (int p = 0; p < LLEP_NUM_PHASES; ++p) c->phase_ms[p] = 0.0;
+    c->calls = c->launches = c->gemm_rows = 0;
+  }
   return LLEP_OK;
 }
 

@@ -40,6 +40,14 @@ class Shape(ctypes.Structure):
                 ("d_ff", ctypes.c_int32), ("world_size", ctypes.c_int32)]
 
 
+PHASES = ("route", "exchange", "plan", "dispatch", "gemm1", "gemm2", "combine")
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * 7), ("calls", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("gemm_rows", ctypes.c_int64)]
+
+
 class Requirements(ctypes.Structure):
     _fields_ = [("rows_needed", ctypes.c_int64), ("foreign_needed", ctypes.c_int32), ("fits", ctypes.c_int32),
                 ("my_rows", ctypes.c_int64), ("my_groups", ctypes.c_int32), ("fallback_ep", ctypes.c_int32),
@@ -64,6 +72,8 @@ _SIGS = {
                                     ctypes.POINTER(Requirements), _vp]),
     "llep_moe_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "llep_debug_copy": (ctypes.c_int, [_vp, _i32, _vp, _i64, _vp]),
+    "llep_context_set_timing": (ctypes.c_int, [_vp, _i32]),
+    "llep_context_stats": (ctypes.c_int, [_vp, ctypes.c_void_p, _i32]),
     "llep_grouped_gemm": (ctypes.c_int, [_i32, _vp, _i64, _i32, _vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
 }
 EXPORTS = tuple(_SIGS)
@@ -206,6 +216,15 @@ class Context:
         _check(_lib.llep_context_reserve(self._h, int(rows), int(foreign)))
         if self.P > 1:
             self.exchange_handles()
+
+    def set_timing(self, on: bool = True) -> None:
+        _check(_lib.llep_context_set_timing(self._h, int(on)))
+
+    def stats(self, reset: bool = False) -> dict:
+        st = Stats()
+        _check(_lib.llep_context_stats(self._h, ctypes.byref(st), int(reset)))
+        return {"ms": dict(zip(PHASES, list(st.ms))), "calls": int(st.calls),
+                "kernel_launches": int(st.kernel_launches), "gemm_rows": int(st.gemm_rows)}
 
     def device_bytes(self) -> int:
         return int(_lib.llep_context_device_bytes(self._h))

@@ -220,8 +220,8 @@ def cpu_baseline(shape, hot, nhot, budget_s=12.0, max_tokens=8192):
 
     for e in np.unique(ids[keep[:max_tokens]]):
         weights(int(e))
-    xb = W.tokens_bits(shape.tokens_per_rank, shape.d_model, 0, SEED)
-    x = W.bf16_bits_to_f64(xb)
+    last = int(keep[:max_tokens].max()) + 1 if keep.size else 1
+    x = W.bf16_bits_to_f64(W.tokens_bits(last, shape.d_model, 0, SEED))  # rows 0..last-1
     done, t_total, chunk = 0, 0.0, 256
     O3.moe_forward(x[keep[:16]], ids[keep[:16]], gates[keep[:16]], weights)  # BLAS warm-up
     while done < min(max_tokens, keep.size) and t_total < budget_s:

@@ -4,7 +4,8 @@
 
 The ranks bootstrap a gloo process group on 127.0.0.1 (plumbing only: it carries the 64-byte CUDA
 IPC handles); all data moves through the library's peer-mapped arenas and device barriers.
-Each rank writes OUTDIR/rank{p}.npz with its LLEP output, EP output and plan blob."""
+Each rank writes OUTDIR/rank{p}.npz with its LLEP output, EP output (the first SAMPLE rows if given),
+the plan blob and whether the whole LLEP and EP outputs are bitwise equal."""
 import os
 import sys
 
@@ -15,7 +16,7 @@ sys.path.insert(0, os.path.dirname(HERE))
 sys.path.insert(0, HERE)
 
 
-def worker(rank, P, cfg, pct, nhot, outdir):
+def worker(rank, P, cfg, pct, nhot, outdir, sample):
     import torch
     import torch.distributed as dist
     import layer_case as LC
@@ -27,7 +28,7 @@ def worker(rank, P, cfg, pct, nhot, outdir):
     torch.cuda.set_device(dev)
     sh0 = W.CONFIGS[cfg]
     sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, P)
-    x, ids, gates, w13, w2, _, _ = LC.rank_inputs(sh, rank, pct, nhot, 21, f"cuda:{dev}")
+    x, ids, gates, w13, w2, _, _ = LC.rank_inputs(sh, rank, None if pct == 0 else pct, nhot, 21, f"cuda:{dev}")
     ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, P, rank, dev, sh.tokens_per_rank)
     out_llep = ctx(x, ids, gates, w13, w2)
     plan = ctx.prepare(ids)[0]          # plan of the LLEP call (deterministic)
@@ -36,8 +37,10 @@ def worker(rank, P, cfg, pct, nhot, outdir):
     out_ep = ctx(x, ids, gates, w13, w2, ep=True)
     torch.cuda.synchronize()
     assert torch.equal(out_llep, out_llep2), "iteration-to-iteration mismatch"
-    np.savez(os.path.join(outdir, f"rank{rank}.npz"), llep=out_llep.float().cpu().numpy(),
-             ep=out_ep.float().cpu().numpy(), plan=plan_np)
+    n = sample if sample > 0 else out_llep.shape[0]
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), llep=out_llep[:n].float().cpu().numpy(),
+             ep=out_ep[:n].float().cpu().numpy(), plan=plan_np,
+             same=np.array(bool(torch.equal(out_llep, out_ep))))
     dist.barrier()
     ctx.close()
     dist.destroy_process_group()
@@ -46,4 +49,5 @@ def worker(rank, P, cfg, pct, nhot, outdir):
 if __name__ == "__main__":
     import torch.multiprocessing as mp
     P, cfg, pct, nhot, outdir = int(sys.argv[1]), sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), sys.argv[5]
-    mp.spawn(worker, args=(P, cfg, pct, nhot, outdir), nprocs=P, join=True)
+    sample = int(sys.argv[6]) if len(sys.argv) > 6 else 0
+    mp.spawn(worker, args=(P, cfg, pct, nhot, outdir, sample), nprocs=P, join=True)

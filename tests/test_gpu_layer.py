@@ -108,4 +108,57 @@ def test_multiprocess_p2_p4_one_gpu(L, tmp_path):
                 mr, l2 = LC.errors(res[p][key].astype(np.float64), ref)
                 assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (P, p, key, mr, l2)
             # same kernels, fixed K-loop and slot order -> LLEP == EP bitwise (reading R28)
-            assert np.array_equal(res[p]["llep"], res[p]["ep"])
+            assert np.array_equal(res[p]["llep"], res[p]["ep"]) and bool(res[p]["same"])
+
+
+def test_g120_p1_sampled_parity(L):
+    """BASELINE config G120 at the N=1 bench launch configuration (P=1, 32K tokens, 95 %/1):
+    sampled outputs vs O3 (tokens whose experts all lie in 0..15, plus the first rows)."""
+    sh0 = W.CONFIGS["g120"]
+    sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, 1)
+    seed = 31
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, 95, 1, seed, "cuda")
+    ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, 1, 0, 0, sh.tokens_per_rank)
+    out = ctx(x, ids, gates, w13, w2)
+    torch.cuda.synchronize()
+    ok = np.nonzero((ids_np < 16).all(1))[0]
+    rows = np.unique(np.concatenate([ok[:40], ok[-24:], [0]]))
+    ref = LC.oracle_rank_output(sh, 0, ids_np, g_np, seed, rows=rows)
+    mr, l2 = LC.errors(_to_np(out[torch.from_numpy(rows).cuda()]), ref)
+    assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (mr, l2)
+    ctx.close()
+
+
+@pytest.mark.parametrize("pct,nhot", [(95, 1), (0, 0)])
+def test_g120_p8_processes_one_gpu(L, tmp_path, pct, nhot):
+    """G120 at its N=8 launch configuration: 8 ranks (processes sharing cuda:0, CUDA-IPC arenas),
+    32K tokens/rank, λ=1.3 α=1 m=1024.  Plan == oracle on every rank, 7 weight transfers at 95 %/1
+    (EP fallback when balanced), sampled outputs vs O3, LLEP == EP bitwise on every full output."""
+    from oracle import planner as O1
+    from oracle import schedule as O2
+    P, S = 8, 48
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29600 + pct))
+    cmd = [sys.executable, os.path.join(HERE, "mp_layer_worker.py"), str(P), "g120", str(pct), str(nhot),
+           str(tmp_path), str(S)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = [np.load(os.path.join(tmp_path, f"rank{p}.npz")) for p in range(P)]
+    sh0 = W.CONFIGS["g120"]
+    sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, P)
+    hot = None if pct == 0 else pct
+    ids_all = [W.routing_ids(sh, p, hot, nhot, 21) for p in range(P)]
+    C = O2.load_matrix(ids_all, sh.n_experts)
+    ref_plan = O1.plan(C.sum(0).tolist(), P)
+    plans = [bytes(r_["plan"].tobytes()) for r_ in res]
+    assert all(p == plans[0] for p in plans)
+    dp = L.parse_plan(plans[0])
+    assert [list(A) for A in dp.chunks] == [list(A) for A in ref_plan.chunks]
+    assert len(ref_plan.transfers) == (7 if pct else 0) and dp.fallback == (pct == 0)
+    w = LC.OracleWeights(sh.d_model, sh.d_ff, 21)
+    rows = np.arange(S)
+    for p in range(P):
+        ref = LC.oracle_rank_output(sh, p, ids_all[p], W.gate_weights(sh.tokens_per_rank, sh.top_k, p, 21), 21,
+                                    rows=rows, weights=w)
+        mr, l2 = LC.errors(res[p]["llep"].astype(np.float64), ref)
+        assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (p, mr, l2)
+        assert bool(res[p]["same"])

@@ -95,12 +95,18 @@ def dist_setup(n_gpus: int):
     if world != n_gpus:
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
     group = None
+    if os.environ.get("LLEP_BENCH_SHARE_GPU") == "1":
+        local = 0  # test mode: all ranks on cuda:0 (CUDA IPC between processes of one device)
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("LLEP_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
     return world, rank, local, group
 
@@ -110,7 +116,8 @@ def max_over_ranks(v: float, world: int) -> float:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -303,7 +310,8 @@ def gpu_main(args):
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(args.config, {}).get("gemm1_dram_bytes_per_launch")
+            tj = json.load(f).get(f"{args.config}_p{world}_{W.scenario_name(hot, args.nhot)}", {})
+            traffic = tj.get("gemm1_dram_bytes_per_launch")
     step_ms = ll["ms_per_step"]
     value = world * B / (step_ms / 1e3)
     line = {

@@ -4,6 +4,7 @@
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -187,6 +188,8 @@ struct llep_context {
   int32_t *rows_on = nullptr, *chunk_row = nullptr, *foreign_slot = nullptr;
   int32_t *dev_padded = nullptr, *dev_foreign = nullptr;
   Group *groups = nullptr;
+  int32_t *sched = nullptr;
+  int64_t sched_cap = 0;
   LayoutSummary *summary = nullptr;
   LayoutSummary *summary_host = nullptr;  // pinned
   int32_t *err_host = nullptr;            // pinned
@@ -394,6 +397,9 @@ llep_status llep_context_create(const llep_shape *s, int32_t rank, int32_t devic
   if (!e) e = A(&c->dev_padded, sizeof(int32_t) * P);
   if (!e) e = A(&c->dev_foreign, sizeof(int32_t) * P);
   if (!e) e = A(&c->groups, sizeof(Group) * kMaxGroups);
+  // worst case: every slot of every rank lands on this device, plus one partial block per group
+  c->sched_cap = ((int64_t)P * slots + kRowAlign - 1) / kRowAlign + kMaxGroups;
+  if (!e) e = A(&c->sched, sizeof(int32_t) * c->sched_cap);
   if (!e) e = A(&c->summary, sizeof(LayoutSummary));
   if (!e) e = A(&c->d_ptrs, sizeof(void *) * 4 * P);
   if (!e) e = cudaMemset(c->err, 0, sizeof(int32_t) * 4);
@@ -424,7 +430,7 @@ void llep_context_destroy(llep_context *c) {
   close_peers(c);
   void *ptrs[] = {c->tile_cnt, c->tile_off, c->cnt, c->local_rank, c->slot_dst, c->err,
                   c->lm_local, c->rows_on, c->chunk_row, c->foreign_slot, c->dev_padded,
-                  c->dev_foreign, c->groups, c->summary, c->d_ptrs, c->act, c->arena};
+                  c->dev_foreign, c->groups, c->sched, c->summary, c->d_ptrs, c->act, c->arena};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->summary_host) cudaFreeHost(c->summary_host);
@@ -524,6 +530,8 @@ static llep_status run_layout(llep_context *c, const void *plan, cudaStream_t s)
   la.dev_padded = c->dev_padded;
   la.dev_foreign = c->dev_foreign;
   la.summary = c->summary;
+  la.sched = c->sched;
+  la.sched_cap = c->sched_cap;
   LLEP_CUDA(launch_layout(la, s));
   ++c->launches;
   return LLEP_OK;
@@ -686,6 +694,7 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   g1.n_foreign = c->arena_foreign;
   g1.nout = H;
   g1.groups = c->groups;
+  g1.sched = getenv("LLEP_GEMM_GROUP_ORDER") ? nullptr : c->sched;
   g1.n_groups_dev = nullptr;
   g1.n_groups_host = sum.my_groups;
   g1.gate = nullptr;
@@ -789,10 +798,27 @@ llep_status llep_grouped_gemm(int32_t mode, const uint16_t *a, int64_t rows, int
     mb += (q[2] + kRowAlign - 1) / kRowAlign;
     // mblk_start counts only this group's blocks: rows between groups are skipped
   }
+  // m-block schedule, same interleave as the layout kernel
+  int64_t nb = 0, ns = 0;
+  std::vector<int64_t> before(std::max(n_groups, 1));
+  for (int i = 0; i < n_groups; ++i) {
+    const int b = (g[i].n_rows + kRowAlign - 1) / kRowAlign;
+    if (b > kSmallGroupBlocks) { before[i] = nb; nb += b; }
+    else { before[i] = ns; ns += b; }
+  }
+  std::vector<int32_t> sched(std::max<int64_t>(mb, 1));
+  for (int i = 0; i < n_groups; ++i) {
+    const int b = (g[i].n_rows + kRowAlign - 1) / kRowAlign;
+    for (int m = 0; m < b; ++m)
+      sched[interleave_pos(b > kSmallGroupBlocks, before[i] + m, nb, ns)] = sched_pack(i, m);
+  }
   cudaStream_t s = (cudaStream_t)stream;
   Group *dg = nullptr;
+  int32_t *dsched = nullptr;
   LLEP_CUDA(cudaMallocAsync(&dg, sizeof(Group) * g.size(), s));
   LLEP_CUDA(cudaMemcpyAsync(dg, g.data(), sizeof(Group) * g.size(), cudaMemcpyHostToDevice, s));
+  LLEP_CUDA(cudaMallocAsync(&dsched, sizeof(int32_t) * sched.size(), s));
+  LLEP_CUDA(cudaMemcpyAsync(dsched, sched.data(), sizeof(int32_t) * sched.size(), cudaMemcpyHostToDevice, s));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -807,6 +833,7 @@ llep_status llep_grouped_gemm(int32_t mode, const uint16_t *a, int64_t rows, int
   ga.n_foreign = 0;
   ga.nout = nout;
   ga.groups = dg;
+  ga.sched = getenv("LLEP_GEMM_GROUP_ORDER") ? nullptr : dsched;  // A/B switch for the schedule
   ga.n_groups_dev = nullptr;
   ga.n_groups_host = n_groups;
   ga.gate = gate;
@@ -814,6 +841,7 @@ llep_status llep_grouped_gemm(int32_t mode, const uint16_t *a, int64_t rows, int
   ga.num_sms = sms;
   llep_status st = n_groups > 0 ? run_grouped_gemm(ga, s) : LLEP_OK;
   cudaFreeAsync(dg, s);
+  cudaFreeAsync(dsched, s);
   return st;
 }
 

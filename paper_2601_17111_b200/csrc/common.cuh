@@ -44,6 +44,26 @@ __host__ __device__ inline PlanLayout plan_layout(int32_t N, int32_t P) {
   return L;
 }
 
+// GEMM m-block schedule.  Groups with few 128-row blocks stream a whole expert's weights for
+// little work (weight-bandwidth bound); their blocks are spread evenly among the blocks of large
+// groups so the persistent GEMM overlaps that streaming with compute-bound tiles.
+constexpr int kSmallGroupBlocks = 2;
+// Position of the idx-th block of its class when nb "big" and ns "small" blocks are merged
+// evenly: keys (2k+1)*ns for big block k, (2j+1)*nb for small block j, ties -> big first.
+__host__ __device__ inline int64_t interleave_pos(bool big, int64_t idx, int64_t nb, int64_t ns) {
+  if (big) {
+    if (ns == 0) return idx;
+    const int64_t c = ((2 * idx + 1) * ns - 1) / nb;
+    const int64_t cnt = (c + 1) / 2;
+    return idx + (cnt < ns ? cnt : ns);
+  }
+  if (nb == 0) return idx;
+  const int64_t c = ((2 * idx + 1) * nb) / ns;
+  const int64_t cnt = (c + 1) / 2;
+  return idx + (cnt < nb ? cnt : nb);
+}
+__host__ __device__ inline int32_t sched_pack(int32_t g, int32_t m) { return (g << 20) | m; }
+
 // Group table entry (8 int32) of one expert group a device computes.
 struct Group {
   int32_t expert;      // global expert id
@@ -79,6 +99,8 @@ struct LayoutArgs {
   int32_t *dev_padded;         // [P] padded rows per device
   int32_t *dev_foreign;        // [P] |S_d|
   LayoutSummary *summary;
+  int32_t *sched;              // [sched_cap] this rank's m-block order (sched_pack)
+  int64_t sched_cap;
 };
 
 // kernel launchers (route.cu / plan.cu / gemm.cu)
@@ -134,6 +156,7 @@ struct GemmArgs {
   int32_t n_foreign;
   int32_t nout;              // output columns: H (mode 0) or D (mode 1)
   const Group *groups;       // device
+  const int32_t *sched;      // device m-block order (sched_pack), or nullptr = group order
   const int32_t *n_groups_dev;  // device int (may be nullptr -> n_groups_host)
   int32_t n_groups_host;
   const float *gate;         // [rows] (mode 1)

@@ -36,6 +36,7 @@ struct GemmParams {
   CUtensorMap tmW0;    // native weights [n_native * wrows, kdim]
   CUtensorMap tmW1;    // foreign weights [n_foreign * wrows, kdim]
   const Group *groups;
+  const int32_t *sched;
   const int32_t *n_groups_dev;
   int32_t n_groups_host;
   int32_t kdim, nout, wrows, n_ntiles, wup_off;
@@ -145,18 +146,28 @@ struct TileInfo {
 };
 
 __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int *s_mblk,
-                                                int n_groups, const Group *groups) {
+                                                int n_groups, const Group *groups,
+                                                const int32_t *sched) {
   TileInfo ti;
   const int mb = t / n_ntiles;
   ti.nb = t - mb * n_ntiles;
-  int lo = 0, hi = n_groups - 1;  // last g with s_mblk[g] <= mb
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (s_mblk[mid] <= mb) lo = mid;
-    else hi = mid - 1;
+  int lo, m;
+  if (sched) {                    // interleaved m-block order from the layout step
+    const int32_t e = __ldg(sched + mb);
+    lo = e >> 20;
+    m = e & 0xFFFFF;
+  } else {                        // group order: last g with s_mblk[g] <= mb
+    lo = 0;
+    int hi = n_groups - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_mblk[mid] <= mb) lo = mid;
+      else hi = mid - 1;
+    }
+    m = mb - s_mblk[lo];
   }
   const Group g = groups[lo];
-  ti.row0 = g.row_base + (mb - s_mblk[lo]) * BM;
+  ti.row0 = g.row_base + m * BM;
   ti.row_end = g.row_base + g.n_rows;
   ti.wslot = g.wslot;
   ti.valid = 1;
@@ -220,7 +231,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const TileInfo ti = decode_tile(t, p.n_ntiles, s_mblk, n_groups, p.groups);
+        const TileInfo ti = decode_tile(t, p.n_ntiles, s_mblk, n_groups, p.groups, p.sched);
         const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
         const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
         for (int kb = 0; kb < nk; ++kb) {
@@ -280,7 +291,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      const TileInfo ti = decode_tile(t, p.n_ntiles, s_mblk, n_groups, p.groups);
+      const TileInfo ti = decode_tile(t, p.n_ntiles, s_mblk, n_groups, p.groups, p.sched);
       mbar_wait(smem_u32(tfull + acc), aphase);
       tc_fence_after();
       const int row = ti.row0 + q * 32 + lane;
@@ -403,6 +414,7 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   GemmParams prm;
   memset(&prm, 0, sizeof(prm));
   prm.groups = g.groups;
+  prm.sched = g.sched;
   prm.n_groups_dev = g.n_groups_dev;
   prm.n_groups_host = g.n_groups_host;
   prm.kdim = g.kdim;

@@ -241,6 +241,8 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(LayoutArgs a) {
   const long long *assigned = reinterpret_cast<const long long *>(plan + L.off_assigned);
   __shared__ int sm_err;
   __shared__ int sm_groups, sm_mblocks;
+  __shared__ int sm_before[kMaxGroups];  // blocks of the same class in earlier groups
+  __shared__ int sm_nbig, sm_nsmall;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) sm_err = 0;
   __syncthreads();
@@ -322,6 +324,39 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(LayoutArgs a) {
     }
   }
   __syncthreads();
+  // m-block schedule of this rank's grouped GEMMs: small groups interleaved among big ones
+  if (tid == 0) {
+    int nb = 0, ns = 0;
+    const int G = sm_groups < kMaxGroups ? sm_groups : kMaxGroups;
+    for (int g = 0; g < G; ++g) {
+      const int mb = (a.groups[g].n_rows + kRowAlign - 1) / kRowAlign;
+      if (mb > kSmallGroupBlocks) {
+        sm_before[g] = nb;
+        nb += mb;
+      } else {
+        sm_before[g] = ns;
+        ns += mb;
+      }
+    }
+    sm_nbig = nb;
+    sm_nsmall = ns;
+  }
+  __syncthreads();
+  if (sm_mblocks <= a.sched_cap && sm_groups <= kMaxGroups) {
+    for (int mb = tid; mb < sm_mblocks; mb += kLayoutThreads) {
+      int lo = 0, hi = sm_groups - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.groups[mid].mblk_start <= mb) lo = mid;
+        else hi = mid - 1;
+      }
+      const Group g = a.groups[lo];
+      const int m = mb - g.mblk_start;
+      const bool big = (g.n_rows + kRowAlign - 1) / kRowAlign > kSmallGroupBlocks;
+      const int64_t pos = interleave_pos(big, sm_before[lo] + m, sm_nbig, sm_nsmall);
+      a.sched[pos] = sched_pack(lo, m);
+    }
+  }
   // destination row of each chunk's first token: group base + rows of e's earlier chunks on d
   for (int e = tid; e < N; e += kLayoutThreads) {
     const int nc = n_chunks[e];
@@ -355,7 +390,7 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(LayoutArgs a) {
     s.fallback_ep = hdr->fallback_ep;
     s.force_count = hdr->force_count;
     s.n_transfers = hdr->n_transfers;
-    s.error = sm_err | (sm_groups > kMaxGroups ? 2 : 0);
+    s.error = sm_err | (sm_groups > kMaxGroups ? 2 : 0) | (sm_mblocks > a.sched_cap ? 8 : 0);
     s.pad = 0;
     *a.summary = s;
   }

@@ -1,0 +1,85 @@
+"""Micro-benchmark of the grouped GEMMs through llep_grouped_gemm (C ABI), A/B over env toggles.
+
+    python tools/gemm_bench.py [--layout g120p1|g120p8|uniform|fgemm] [--iters 20]
+
+Group layouts: g120p1 = G120 at P=1 (1 hot group of 124518 rows + 127 groups of 51-52 rows),
+g120p8 = one LLEP device at P=8 (a 124464-row spilled chunk + 16 native groups of ~413 rows),
+fgemm = the paper's F-gemm shape (65536 tokens over E experts)."""
+import argparse
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2601_17111_b200 import llep as L  # noqa: E402
+
+
+def layout(name):
+    if name == "g120p1":
+        return [124518] + [52] * 77 + [51] * 50
+    if name == "g120p8":
+        return [124464] + [413] * 16
+    if name == "uniform":
+        return [1024] * 128
+    if name.startswith("fgemm"):
+        E = int(name[5:] or 16)
+        return [65536 // E] * E
+    raise ValueError(name)
+
+
+def groups_of(sizes, n_weights):
+    g, rb = [], 0
+    for i, n in enumerate(sizes):
+        g.append((i % n_weights, rb, n))
+        rb += (n + 127) // 128 * 128
+    return g, rb
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layout", default="g120p1")
+    ap.add_argument("--D", type=int, default=2880)
+    ap.add_argument("--H", type=int, default=2880)
+    ap.add_argument("--iters", type=int, default=20)
+    args = ap.parse_args()
+    D, H = args.D, args.H
+    sizes = layout(args.layout)
+    E = len(sizes)
+    groups, rows = groups_of(sizes, E)
+    x = torch.randn(rows, D, device="cuda").to(torch.bfloat16)
+    w13 = (torch.randn(E, 2 * H, D, device="cuda") / D ** 0.5).to(torch.bfloat16)
+    w2 = (torch.randn(E, D, H, device="cuda") / H ** 0.5).to(torch.bfloat16)
+    act = torch.empty(rows, H, device="cuda", dtype=torch.bfloat16)
+    y = torch.empty(rows, D, device="cuda", dtype=torch.bfloat16)
+    gate = torch.rand(rows, device="cuda")
+    real = sum(sizes)
+    res = {}
+    for variant in ("interleave", "group_order") * 2:
+        if variant == "group_order":
+            os.environ["LLEP_GEMM_GROUP_ORDER"] = "1"
+        else:
+            os.environ.pop("LLEP_GEMM_GROUP_ORDER", None)
+        for mode in (0, 1):
+            ts = []
+            for it in range(args.iters + 3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                if mode == 0:
+                    L.grouped_gemm(0, x, w13, groups, H, out=act)
+                else:
+                    L.grouped_gemm(1, act, w2, groups, D, gate=gate, out=y)
+                e1.record()
+                torch.cuda.synchronize()
+                if it >= 3:
+                    ts.append(e0.elapsed_time(e1))
+            ms = statistics.median(ts)
+            flops = (4 if mode == 0 else 2) * D * H * real
+            res.setdefault((variant, mode), []).append(ms)
+            print(f"{args.layout:8s} {variant:12s} gemm{mode + 1}: {ms:7.3f} ms  {flops / ms / 1e9:7.1f} TFLOP/s")
+    return res
+
+
+if __name__ == "__main__":
+    main()

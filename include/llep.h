@@ -243,7 +243,8 @@ llep_status llep_debug_copy(llep_context *ctx, int32_t what, void *dst, int64_t 
                             void *stream);
 
 /* Standalone grouped-GEMM entry (kernel tests / micro-bench, the paper's F-gemm shape P:1127):
- * rows of group g occupy [row_base[g], row_base[g]+n_rows[g]) of a, with row_base % 128 == 0.
+ * rows of group g occupy [row_base[g], row_base[g]+n_rows[g]) of a, with row_base % 128 == 0
+ * (% 256 when mode bit 1 is set: 2-CTA cta_group::2 M=256 tiles; mode & 1 selects the epilogue).
  *   mode 0: out[r, 0:Hn] = silu(a W[e][0:Hn]ᵀ) ⊙ (a W[e][Hn:2Hn]ᵀ),  W [E, 2Hn, Kd], out [R, Hn]
  *   mode 1: out[r, 0:Nn] = gate[r] · (a W[e]ᵀ),                      W [E, Nn, Kd],  out [R, Nn]
  * groups: HOST int32 [G*4] = (expert, row_base, n_rows, 0), increasing non-overlapping rows.

@@ -181,6 +181,7 @@ using namespace llep;
 // ====================================================================== context
 struct llep_context {
   int32_t N, K, D, H, P, M, rank, device, num_sms;
+  int32_t row_align = 256;  // 256: 2-CTA GEMM tiles; 128: 1-CTA tiles (LLEP_ROW_ALIGN=128)
   int64_t max_tokens;
   // rank-local scratch
   int32_t *tile_cnt = nullptr, *tile_off = nullptr, *cnt = nullptr, *local_rank = nullptr;
@@ -376,6 +377,7 @@ llep_status llep_context_create(const llep_shape *s, int32_t rank, int32_t devic
   c->device = device;
   c->max_tokens = max_tokens;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (const char *ra = getenv("LLEP_ROW_ALIGN")) c->row_align = atoi(ra) == 128 ? 128 : 256;
   const int64_t slots = std::max<int64_t>(1, max_tokens * c->K);
   const int64_t tiles = (slots + kTileSlots - 1) / kTileSlots;
   auto A = [&](auto **p, size_t bytes) -> cudaError_t {
@@ -414,7 +416,7 @@ llep_status llep_context_create(const llep_shape *s, int32_t rank, int32_t devic
     return cuda_status(e, "llep_context_create");
   }
   // initial arena: every rank's local slots, room for the balanced case
-  const int64_t rows0 = (max_tokens * c->K + (int64_t)c->M * kRowAlign);
+  const int64_t rows0 = (max_tokens * c->K + (int64_t)c->M * c->row_align);
   if ((st = alloc_arena(c, rows0, 1)) != LLEP_OK) {
     llep_context_destroy(c);
     return st;
@@ -532,6 +534,7 @@ static llep_status run_layout(llep_context *c, const void *plan, cudaStream_t s)
   la.summary = c->summary;
   la.sched = c->sched;
   la.sched_cap = c->sched_cap;
+  la.row_align = c->row_align;
   LLEP_CUDA(launch_layout(la, s));
   ++c->launches;
   return LLEP_OK;
@@ -700,6 +703,7 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   g1.gate = nullptr;
   g1.out = c->act;
   g1.num_sms = c->num_sms;
+  g1.row_align = c->row_align;
   if (sum.my_groups > 0 && (st = run_grouped_gemm(g1, s)) != LLEP_OK) return st;
   c->launches += sum.my_groups > 0;
   mark(c, 6, s);
@@ -782,35 +786,37 @@ llep_status llep_grouped_gemm(int32_t mode, const uint16_t *a, int64_t rows, int
                               const uint16_t *w, int32_t n_weights, int32_t nout,
                               const int32_t *groups, int32_t n_groups, const float *gate,
                               uint16_t *out, void *stream) {
+  if (mode < 0 || mode > 3) return invalid("mode must be 0..3");
+  const int ra = (mode & 2) ? 256 : kRowAlign;   // mode bit 1: 2-CTA (cta_group::2) tiles
+  mode &= 1;
   if (!a || !w || !groups || !out || (mode == 1 && !gate)) return invalid("null pointer");
-  if (mode != 0 && mode != 1) return invalid("mode must be 0 or 1");
   if (n_groups < 0 || n_groups > kMaxGroups) return invalid("n_groups out of range");
   std::vector<Group> g(std::max(n_groups, 1));
   int mb = 0;
   for (int i = 0; i < n_groups; ++i) {
     const int32_t *q = groups + 4 * i;
     if (q[0] < 0 || q[0] >= n_weights) return invalid("group expert out of range");
-    if (q[1] % kRowAlign || q[2] < 1 || q[1] + (int64_t)q[2] > rows)
-      return invalid("group rows must start 128-aligned, be nonempty and fit in `rows`");
-    if (i > 0 && q[1] < g[i - 1].row_base + ((g[i - 1].n_rows + kRowAlign - 1) / kRowAlign) * kRowAlign)
+    if (q[1] % ra || q[2] < 1 || q[1] + (int64_t)q[2] > rows)
+      return invalid("group rows must start tile-aligned (128, or 256 for 2-CTA), be nonempty and fit");
+    if (i > 0 && q[1] < g[i - 1].row_base + ((g[i - 1].n_rows + ra - 1) / ra) * ra)
       return invalid("groups must be in increasing, non-overlapping row order");
     g[i] = Group{q[0], q[0], q[1], q[2], mb, {0, 0, 0}};
-    mb += (q[2] + kRowAlign - 1) / kRowAlign;
+    mb += (q[2] + ra - 1) / ra;
     // mblk_start counts only this group's blocks: rows between groups are skipped
   }
   // m-block schedule, same interleave as the layout kernel
   int64_t nb = 0, ns = 0;
   std::vector<int64_t> before(std::max(n_groups, 1));
   for (int i = 0; i < n_groups; ++i) {
-    const int b = (g[i].n_rows + kRowAlign - 1) / kRowAlign;
-    if (b > kSmallGroupBlocks) { before[i] = nb; nb += b; }
+    const int b = (g[i].n_rows + ra - 1) / ra;
+    if (b * ra > kSmallGroupRows) { before[i] = nb; nb += b; }
     else { before[i] = ns; ns += b; }
   }
   std::vector<int32_t> sched(std::max<int64_t>(mb, 1));
   for (int i = 0; i < n_groups; ++i) {
-    const int b = (g[i].n_rows + kRowAlign - 1) / kRowAlign;
+    const int b = (g[i].n_rows + ra - 1) / ra;
     for (int m = 0; m < b; ++m)
-      sched[interleave_pos(b > kSmallGroupBlocks, before[i] + m, nb, ns)] = sched_pack(i, m);
+      sched[interleave_pos(b * ra > kSmallGroupRows, before[i] + m, nb, ns)] = sched_pack(i, m);
   }
   cudaStream_t s = (cudaStream_t)stream;
   Group *dg = nullptr;
@@ -839,6 +845,7 @@ llep_status llep_grouped_gemm(int32_t mode, const uint16_t *a, int64_t rows, int
   ga.gate = gate;
   ga.out = out;
   ga.num_sms = sms;
+  ga.row_align = ra;
   llep_status st = n_groups > 0 ? run_grouped_gemm(ga, s) : LLEP_OK;
   cudaFreeAsync(dg, s);
   cudaFreeAsync(dsched, s);

@@ -47,7 +47,7 @@ __host__ __device__ inline PlanLayout plan_layout(int32_t N, int32_t P) {
 // GEMM m-block schedule.  Groups with few 128-row blocks stream a whole expert's weights for
 // little work (weight-bandwidth bound); their blocks are spread evenly among the blocks of large
 // groups so the persistent GEMM overlaps that streaming with compute-bound tiles.
-constexpr int kSmallGroupBlocks = 2;
+constexpr int kSmallGroupRows = 256;  // groups of at most this many padded rows are "small"
 // Position of the idx-th block of its class when nb "big" and ns "small" blocks are merged
 // evenly: keys (2k+1)*ns for big block k, (2j+1)*nb for small block j, ties -> big first.
 __host__ __device__ inline int64_t interleave_pos(bool big, int64_t idx, int64_t nb, int64_t ns) {
@@ -101,6 +101,7 @@ struct LayoutArgs {
   LayoutSummary *summary;
   int32_t *sched;              // [sched_cap] this rank's m-block order (sched_pack)
   int64_t sched_cap;
+  int32_t row_align;           // group row bases / GEMM M tile: 128 or 256
 };
 
 // kernel launchers (route.cu / plan.cu / gemm.cu)
@@ -162,6 +163,7 @@ struct GemmArgs {
   const float *gate;         // [rows] (mode 1)
   uint16_t *out;             // [rows, nout]
   int32_t num_sms;
+  int32_t row_align;         // 128: 1-CTA M=128 tiles; 256: 2-CTA (cta_group::2) M=256 tiles
 };
 llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s);
 

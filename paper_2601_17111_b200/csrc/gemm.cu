@@ -145,6 +145,7 @@ struct TileInfo {
   int row0, row_end, nb, wslot, valid;
 };
 
+template <int TM = BM>
 __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int *s_mblk,
                                                 int n_groups, const Group *groups,
                                                 const int32_t *sched) {
@@ -167,7 +168,7 @@ __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int *
     m = mb - s_mblk[lo];
   }
   const Group g = groups[lo];
-  ti.row0 = g.row_base + m * BM;
+  ti.row0 = g.row_base + m * TM;
   ti.row_end = g.row_base + g.n_rows;
   ti.wslot = g.wslot;
   ti.valid = 1;
@@ -311,8 +312,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
             __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const float a0 = g[2 * i] / (1.f + __expf(-g[2 * i])) * u[2 * i];
-              const float a1 = g[2 * i + 1] / (1.f + __expf(-g[2 * i + 1])) * u[2 * i + 1];
+              const float a0 = __fdividef(g[2 * i], 1.f + __expf(-g[2 * i])) * u[2 * i];
+              const float a1 = __fdividef(g[2 * i + 1], 1.f + __expf(-g[2 * i + 1])) * u[2 * i + 1];
               h[i] = __floats2bfloat162_rn(a0, a1);
             }
             *reinterpret_cast<uint4 *>(orow + j) = o;
@@ -345,6 +346,243 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
   tc_fence_after();
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(2 * kAccCols)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------------------ 2-CTA variant
+// A CTA pair (cluster of 2, one TPC) computes a 256-row tile with tcgen05.mma.cta_group::2.
+// Each CTA stages its own 128 rows of A and HALF of the B tile (mode 0: CTA0 the W_gate rows,
+// CTA1 the matching W_up rows; mode 1: the two halves of the N tile), so the per-SM shared-memory
+// operand traffic per MMA drops by a third.  The leader (cluster rank 0) issues the MMAs; both
+// CTAs' TMA loads complete on the leader's full barrier; the MMA commits are multicast to both
+// CTAs' empty / accumulator-full barriers; each CTA's epilogue drains its own TMEM lanes (its 128
+// rows of the 256-row accumulator) and arrives on the leader's TMEM-empty barrier.
+template <int BN>
+struct Cfg2 {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int EXTRA = 1024 + 256;
+  static constexpr int STAGES_RAW = (kSmemBudget - EXTRA) / STAGE;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int SMEM = STAGES * STAGE + EXTRA;
+  static_assert(B_BYTES % 1024 == 0, "B half tile must keep 1024-byte swizzle alignment");
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map, uint32_t leader_bar,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+      ::"r"(bar), "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(const __grid_constant__ GemmParams p) {
+  using C = Cfg2<BN>;
+  constexpr int S = C::STAGES;
+  constexpr int TM = 2 * BM;                     // rows per pair tile
+  constexpr int BH = BN / 2;                     // B rows staged by each CTA
+  constexpr int BNO = MODE == 0 ? BN / 2 : BN;   // output columns per tile
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + S * C::A_BYTES;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S * C::STAGE);
+  uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  const int n_groups = p.n_groups_dev ? *p.n_groups_dev : p.n_groups_host;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(smem_u32(full + i), 1);
+      mbar_init(smem_u32(empty + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(tfull + i), 1);
+      mbar_init(smem_u32(tempty + i), 8);        // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmW0)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmW1)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(2 * kAccCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  int total_tiles = 0;
+  if (n_groups > 0) {
+    const Group last = p.groups[n_groups - 1];
+    total_tiles = (last.mblk_start + (last.n_rows + TM - 1) / TM) * p.n_ntiles;
+  }
+  const int nk = (p.kdim + BK - 1) / BK;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < total_tiles; t += n_pairs) {
+        const TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
+        const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
+        const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
+        const int brow = MODE == 0 ? wbase + (int)crank * p.wup_off : wbase + (int)crank * BH;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(smem_u32(empty + stage), phase ^ 1);
+          const uint32_t fl = smem_u32(full + stage);
+          if (leader) mbar_expect_tx(fl, 2 * C::STAGE);
+          const uint32_t fb = mapa_shared(fl, 0);
+          tma_load_2d_pair(smem_u32(sA + stage * C::A_BYTES), &p.tmA, fb, kb * BK, ti.row0 + (int)crank * BM);
+          tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES), wm, fb, kb * BK, brow);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------------------------------------------------------- MMA issuer (leader)
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(TM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair; t < total_tiles; t += n_pairs, ++it) {
+        const int acc = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(smem_u32(tempty + acc), aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(smem_u32(full + stage), phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            tc_mma_pair(d_tmem, smem_desc(a0 + kk * 32), smem_desc(b0 + kk * 32), idesc,
+                        (kb | kk) != 0);
+          tc_commit_pair(smem_u32(empty + stage));
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_pair(smem_u32(tfull + acc));
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;
+    int it = 0;
+    for (int t = pair; t < total_tiles; t += n_pairs, ++it) {
+      const int acc = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      const TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
+      mbar_wait(smem_u32(tfull + acc), aphase);
+      tc_fence_after();
+      const int row = ti.row0 + (int)crank * BM + q * 32 + lane;
+      const bool row_ok = row < ti.row_end;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
+      const int col0 = ti.nb * BNO;
+      if (MODE == 0) {
+        __nv_bfloat16 *orow = p.out + (size_t)row * p.nout + col0;
+#pragma unroll 1
+        for (int j = 0; j < BNO; j += 8) {
+          float g[8], u[8];
+          tmem_ld8(taddr + j, g);
+          tmem_ld8(taddr + BNO + j, u);
+          tmem_ld_wait();
+          if (row_ok && col0 + j < p.nout) {
+            uint4 o;
+            __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float a0 = __fdividef(g[2 * i], 1.f + __expf(-g[2 * i])) * u[2 * i];
+              const float a1 = __fdividef(g[2 * i + 1], 1.f + __expf(-g[2 * i + 1])) * u[2 * i + 1];
+              h[i] = __floats2bfloat162_rn(a0, a1);
+            }
+            *reinterpret_cast<uint4 *>(orow + j) = o;
+          }
+        }
+      } else {
+        const float gs = row_ok ? p.gate[row] : 0.f;
+        __nv_bfloat16 *orow = p.out + (size_t)row * p.nout + col0;
+#pragma unroll 1
+        for (int j = 0; j < BNO; j += 8) {
+          float v[8];
+          tmem_ld8(taddr + j, v);
+          tmem_ld_wait();
+          if (row_ok && col0 + j < p.nout) {
+            uint4 o;
+            __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(gs * v[2 * i], gs * v[2 * i + 1]);
+            *reinterpret_cast<uint4 *>(orow + j) = o;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(tempty + acc), 0));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(2 * kAccCols)
                  : "memory");
   }
@@ -404,6 +642,43 @@ llep_status launch(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
   return LLEP_OK;
 }
 
+template <int BN, int MODE>
+llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
+  using C = Cfg2<BN>;
+  auto kern = grouped_gemm_2cta_kernel<BN, MODE>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    LLEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  const int box_w = BN / 2;
+  const int wrows = MODE == 0 ? 2 * g.nout : g.nout;
+  if (!make_map(&prm.tmA, g.a, g.a_rows, g.kdim, BM) ||
+      !make_map(&prm.tmW0, g.w_native, (int64_t)g.n_native * wrows, g.kdim, box_w) ||
+      !make_map(&prm.tmW1, g.w_foreign ? g.w_foreign : g.w_native,
+                (int64_t)(g.w_foreign ? g.n_foreign : g.n_native) * wrows, g.kdim, box_w)) {
+    set_error("cuTensorMapEncodeTiled failed (alignment: kdim %% 8 == 0, 16-byte aligned bases)");
+    return LLEP_ERR_CUDA;
+  }
+  prm.wrows = wrows;
+  prm.wup_off = MODE == 0 ? g.nout : 0;
+  prm.n_ntiles = (g.nout + (MODE == 0 ? BN / 2 : BN) - 1) / (MODE == 0 ? BN / 2 : BN);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(g.num_sms & ~1));
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LLEP_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
+  return LLEP_OK;
+}
+
 }  // namespace
 
 llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
@@ -421,6 +696,18 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   prm.nout = g.nout;
   prm.gate = g.gate;
   prm.out = reinterpret_cast<__nv_bfloat16 *>(g.out);
+  if (g.row_align == 2 * BM) {   // 2-CTA pair tiles (groups 256-row aligned)
+    if (g.mode == 0) {
+      if (g.nout % 128 == 0) return launch_pair<256, 0>(g, prm, s);
+      if (g.nout % 120 == 0) return launch_pair<240, 0>(g, prm, s);
+      if (g.nout % 96 == 0) return launch_pair<192, 0>(g, prm, s);
+      return launch_pair<256, 0>(g, prm, s);
+    }
+    if (g.nout % 256 == 0) return launch_pair<256, 1>(g, prm, s);
+    if (g.nout % 240 == 0) return launch_pair<240, 1>(g, prm, s);
+    if (g.nout % 192 == 0) return launch_pair<192, 1>(g, prm, s);
+    return launch_pair<256, 1>(g, prm, s);
+  }
   // tile width: widest instantiated N that divides the output (else masked tail tiles)
   if (g.mode == 0) {
     if (g.nout % 128 == 0) return launch<256, 0>(g, prm, s);

@@ -277,8 +277,9 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(LayoutArgs a) {
         const bool in = e < N && (pass == 0 ? native : !native);
         const int rows = in ? a.rows_on[(size_t)e * P + d] : 0;
         const bool has = rows > 0;
-        const int padded = (rows + kRowAlign - 1) / kRowAlign * kRowAlign;
-        const int mblk = padded / kRowAlign;
+        const int ra = a.row_align;
+        const int padded = (rows + ra - 1) / ra * ra;
+        const int mblk = padded / ra;
         int inc = padded, incm = mblk;
         for (int o = 1; o < 32; o <<= 1) {
           int u = __shfl_up_sync(0xffffffffu, inc, o);
@@ -329,8 +330,8 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(LayoutArgs a) {
     int nb = 0, ns = 0;
     const int G = sm_groups < kMaxGroups ? sm_groups : kMaxGroups;
     for (int g = 0; g < G; ++g) {
-      const int mb = (a.groups[g].n_rows + kRowAlign - 1) / kRowAlign;
-      if (mb > kSmallGroupBlocks) {
+      const int mb = (a.groups[g].n_rows + a.row_align - 1) / a.row_align;
+      if (mb * a.row_align > kSmallGroupRows) {
         sm_before[g] = nb;
         nb += mb;
       } else {
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(LayoutArgs a) {
       }
       const Group g = a.groups[lo];
       const int m = mb - g.mblk_start;
-      const bool big = (g.n_rows + kRowAlign - 1) / kRowAlign > kSmallGroupBlocks;
+      const bool big = (g.n_rows + a.row_align - 1) / a.row_align * a.row_align > kSmallGroupRows;
       const int64_t pos = interleave_pos(big, sm_before[lo] + m, sm_nbig, sm_nsmall);
       a.sched[pos] = sched_pack(lo, m);
     }

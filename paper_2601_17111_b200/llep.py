@@ -273,16 +273,18 @@ class Context:
         return t
 
 
-def grouped_gemm(mode: int, a, w, groups: Sequence[Tuple[int, int, int]], nout: int, gate=None, out=None):
+def grouped_gemm(mode: int, a, w, groups: Sequence[Tuple[int, int, int]], nout: int, gate=None, out=None,
+                 pair: bool = False):
     """llep_grouped_gemm: groups = [(expert, row_base, n_rows)] (host), a [rows, kdim] bf16,
-    mode 0: w [E, 2*nout, kdim] -> SwiGLU [rows, nout]; mode 1: w [E, nout, kdim] -> gate*(a wᵀ)."""
+    mode 0: w [E, 2*nout, kdim] -> SwiGLU [rows, nout]; mode 1: w [E, nout, kdim] -> gate*(a wᵀ).
+    pair=True: 2-CTA (cta_group::2) 256-row tiles, row bases must be multiples of 256."""
     import torch
     rows, kdim = a.shape
     if out is None:
         out = torch.zeros((rows, nout), dtype=torch.bfloat16, device=a.device)
     g = np.asarray([[e, rb, n, 0] for (e, rb, n) in groups], dtype=np.int32).reshape(-1)
     g = np.ascontiguousarray(g)
-    _check(_lib.llep_grouped_gemm(mode, a.data_ptr(), rows, kdim, w.data_ptr(), w.shape[0], nout,
+    _check(_lib.llep_grouped_gemm(mode | (2 if pair else 0), a.data_ptr(), rows, kdim, w.data_ptr(), w.shape[0], nout,
                                   g.ctypes.data, len(groups), gate.data_ptr() if gate is not None else None,
                                   out.data_ptr(), _stream_ptr()))
     return out

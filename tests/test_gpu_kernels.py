@@ -65,6 +65,7 @@ def _ref_gemm(mode, a, w, groups, nout, gate):
     return out
 
 
+@pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("mode,kdim,nout", [
     (0, 256, 512),    # TINY GEMM1 (BN=256)
     (1, 512, 256),    # TINY GEMM2
@@ -75,22 +76,23 @@ def _ref_gemm(mode, a, w, groups, nout, gate):
     (0, 192, 200),    # ragged: masked tail tile, partial K block
     (1, 200, 136),
 ])
-def test_grouped_gemm(L, mode, kdim, nout):
+def test_grouped_gemm(L, mode, kdim, nout, pair):
     g = torch.Generator(device="cuda").manual_seed(kdim * 7 + nout)
     E = 3
-    sizes = [1, 300, 0, 129, 128, 77]
+    sizes = [1, 300, 0, 129, 128, 77, 600]
+    ra = 256 if pair else 128
     groups, rb = [], 0
     for i, n in enumerate(sizes):
         if n == 0:
             continue
         groups.append((i % E, rb, n))
-        rb += (n + 127) // 128 * 128
+        rb += (n + ra - 1) // ra * ra
     rows = rb + 128
     a = (torch.randn((rows, kdim), generator=g, device="cuda") ).to(torch.bfloat16)
     wr = 2 * nout if mode == 0 else nout
     w = (torch.randn((E, wr, kdim), generator=g, device="cuda") / kdim ** 0.5).to(torch.bfloat16)
     gate = torch.rand((rows,), generator=g, device="cuda") if mode == 1 else None
-    out = L.grouped_gemm(mode, a, w, groups, nout, gate)
+    out = L.grouped_gemm(mode, a, w, groups, nout, gate, pair=pair)
     torch.cuda.synchronize()
     ref = _ref_gemm(mode, a, w, groups, nout, gate)
     for (e, rb, n) in groups:

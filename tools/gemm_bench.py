@@ -29,11 +29,11 @@ def layout(name):
     raise ValueError(name)
 
 
-def groups_of(sizes, n_weights):
+def groups_of(sizes, n_weights, ra=128):
     g, rb = [], 0
     for i, n in enumerate(sizes):
         g.append((i % n_weights, rb, n))
-        rb += (n + 127) // 128 * 128
+        rb += (n + ra - 1) // ra * ra
     return g, rb
 
 
@@ -43,11 +43,12 @@ def main():
     ap.add_argument("--D", type=int, default=2880)
     ap.add_argument("--H", type=int, default=2880)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--variants", default="cta1,cta2")
     args = ap.parse_args()
     D, H = args.D, args.H
     sizes = layout(args.layout)
     E = len(sizes)
-    groups, rows = groups_of(sizes, E)
+    groups, rows = groups_of(sizes, E, 256)
     x = torch.randn(rows, D, device="cuda").to(torch.bfloat16)
     w13 = (torch.randn(E, 2 * H, D, device="cuda") / D ** 0.5).to(torch.bfloat16)
     w2 = (torch.randn(E, D, H, device="cuda") / H ** 0.5).to(torch.bfloat16)
@@ -56,20 +57,21 @@ def main():
     gate = torch.rand(rows, device="cuda")
     real = sum(sizes)
     res = {}
-    for variant in ("interleave", "group_order") * 2:
+    for variant in args.variants.split(",") * 2:
         if variant == "group_order":
             os.environ["LLEP_GEMM_GROUP_ORDER"] = "1"
         else:
             os.environ.pop("LLEP_GEMM_GROUP_ORDER", None)
+        pair = variant == "cta2"
         for mode in (0, 1):
             ts = []
             for it in range(args.iters + 3):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 if mode == 0:
-                    L.grouped_gemm(0, x, w13, groups, H, out=act)
+                    L.grouped_gemm(0, x, w13, groups, H, out=act, pair=pair)
                 else:
-                    L.grouped_gemm(1, act, w2, groups, D, gate=gate, out=y)
+                    L.grouped_gemm(1, act, w2, groups, D, gate=gate, out=y, pair=pair)
                 e1.record()
                 torch.cuda.synchronize()
                 if it >= 3:

@@ -173,35 +173,67 @@ def run_mode(L, shape, rank, local, world, group, inputs, ep: bool, steps: int, 
 
 
 def run_e2e(L, ctx, shape, host, dev, steps, warmup, world, ep=False):
-    """Public API end to end: pinned host inputs -> H2D -> layer -> D2H of the output, every step."""
+    """Public API end to end: every step copies its inputs from pinned host memory (H2D), runs the
+    layer (llep_prepare + llep_moe_forward) and reads the output back (D2H).  Double-buffered: the
+    H2D of step i+1 and the D2H of step i-1 run on copy streams while step i computes."""
     import torch
     x_h, ids_h, g_h = host
-    x, ids, gates, w13, w2 = dev
-    out = torch.empty_like(x)
-    out_h = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
-    plan_buf = torch.empty(L.plan_bytes(shape.n_experts, world), dtype=torch.uint8, device=x.device)
+    _, _, _, w13, w2 = dev
+    nb = 2
+    xs = [torch.empty(x_h.shape, dtype=x_h.dtype, device="cuda") for _ in range(nb)]
+    idss = [torch.empty(ids_h.shape, dtype=ids_h.dtype, device="cuda") for _ in range(nb)]
+    gs = [torch.empty(g_h.shape, dtype=g_h.dtype, device="cuda") for _ in range(nb)]
+    outs = [torch.empty(x_h.shape, dtype=torch.bfloat16, device="cuda") for _ in range(nb)]
+    outs_h = [torch.empty(x_h.shape, dtype=torch.bfloat16, pin_memory=True) for _ in range(nb)]
+    plans = [torch.empty(L.plan_bytes(shape.n_experts, world), dtype=torch.uint8, device="cuda") for _ in range(nb)]
+    comp = torch.cuda.current_stream()
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_h2d = [torch.cuda.Event() for _ in range(nb)]
+    ev_comp = [torch.cuda.Event() for _ in range(nb)]
+    ev_d2h = [torch.cuda.Event() for _ in range(nb)]
+    for b in range(nb):
+        ev_comp[b].record(comp)
+        ev_d2h[b].record(comp)
 
-    def step():
-        x.copy_(x_h, non_blocking=True)
-        ids.copy_(ids_h, non_blocking=True)
-        gates.copy_(g_h, non_blocking=True)
-        ctx(x, ids, gates, w13, w2, ep=ep, plan_out=plan_buf, out=out)
-        out_h.copy_(out, non_blocking=True)
+    def load(i):
+        b = i % nb
+        with torch.cuda.stream(h2d):
+            h2d.wait_event(ev_comp[b])          # step i-2 finished reading this buffer
+            xs[b].copy_(x_h, non_blocking=True)
+            idss[b].copy_(ids_h, non_blocking=True)
+            gs[b].copy_(g_h, non_blocking=True)
+            ev_h2d[b].record(h2d)
 
-    for _ in range(warmup):
-        step()
+    def compute(i):
+        b = i % nb
+        comp.wait_event(ev_h2d[b])
+        comp.wait_event(ev_d2h[b])              # D2H of step i-2 done with outs[b]
+        ctx(xs[b], idss[b], gs[b], w13, w2, ep=ep, plan_out=plans[b], out=outs[b])
+        ev_comp[b].record(comp)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(ev_comp[b])
+            outs_h[b].copy_(outs[b], non_blocking=True)
+            ev_d2h[b].record(d2h)
+
+    def run(n):
+        load(0)
+        for i in range(n):
+            if i + 1 < n:
+                load(i + 1)
+            compute(i)
+        comp.wait_stream(d2h)
+
+    run(warmup)
     barrier(world)
-    s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s)
-    for _ in range(steps):
-        step()
-    e1.record(s)
+    e0.record(comp)
+    run(steps)
+    e1.record(comp)
     barrier(world)
     ms = max_over_ranks(e0.elapsed_time(e1), world)
-    h2d = x_h.numel() * 2 + ids_h.numel() * 4 + g_h.numel() * 4
-    d2h = out_h.numel() * 2
-    return ms / steps, h2d, d2h
+    bytes_h2d = x_h.numel() * 2 + ids_h.numel() * 4 + g_h.numel() * 4
+    bytes_d2h = outs_h[0].numel() * 2
+    return ms / steps, bytes_h2d, bytes_d2h
 
 
 def cpu_baseline(shape, hot, nhot, budget_s=12.0, max_tokens=8192):
@@ -274,7 +306,9 @@ def gpu_main(args):
         dev_bufs = (torch.empty_like(x), torch.empty_like(ids), torch.empty_like(gates), w13, w2)
         ms_e2e, h2d, d2h = run_e2e(L, ll_ctx, shape, host, dev_bufs, max(3, args.steps // 2), 2, world)
         e2e = {"value": world * B / (ms_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e}
+               "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
+               "note": "pinned host -> device inputs and device -> host output every step, "
+                       "double-buffered on copy streams"}
     ll_ctx.close()
 
     sweep = []
@@ -340,6 +374,11 @@ def gpu_main(args):
                      "flops_per_launch": g1_flops, "ms_per_launch": g1_ms,
                      "gemm2_tflops": g2_flops / (g2_ms / 1e3) / 1e12 if g2_ms > 0 else 0.0,
                      "layer_tflops": (g1_flops + g2_flops) / (step_ms / 1e3) / 1e12},
+        "hbm": {"dispatch_gbs": (B * D * 2 + B * K * (2 * D + 4)) / (st["ms"]["dispatch"] / calls / 1e3) / 1e9
+                if world == 1 and st["ms"]["dispatch"] > 0 else None,
+                "combine_gbs": (B * K * 2 * D + B * D * 2) / (st["ms"]["combine"] / calls / 1e3) / 1e9
+                if world == 1 and st["ms"]["combine"] > 0 else None,
+                "peak": peaks["hbm_gbs"], "note": "algorithmic bytes / phase time (P=1: all rows local)"},
         "gpu_launches": st["kernel_launches"],
         "clocks": ll["clocks"],
     }

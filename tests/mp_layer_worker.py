@@ -29,9 +29,11 @@ def worker(rank, P, cfg, pct, nhot, outdir, sample):
     sh0 = W.CONFIGS[cfg]
     sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, P)
     x, ids, gates, w13, w2, _, _ = LC.rank_inputs(sh, rank, None if pct == 0 else pct, nhot, 21, f"cuda:{dev}")
+    alpha, m, lam = (float(v) for v in os.environ.get("LLEP_TEST_PARAMS", "1,1024,1.3").split(","))
+    m = int(m)
     ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, P, rank, dev, sh.tokens_per_rank)
-    out_llep = ctx(x, ids, gates, w13, w2)
-    plan = ctx.prepare(ids)[0]          # plan of the LLEP call (deterministic)
+    out_llep = ctx(x, ids, gates, w13, w2, alpha, m, lam)
+    plan = ctx.prepare(ids, alpha, m, lam)[0]          # plan of the LLEP call (deterministic)
     plan_np = plan.cpu().numpy()
     out_llep2 = ctx.forward(x, ids, gates, w13, w2, plan)   # second iteration on the same arena
     out_ep = ctx(x, ids, gates, w13, w2, ep=True)

@@ -111,6 +111,59 @@ def test_multiprocess_p2_p4_one_gpu(L, tmp_path):
             assert np.array_equal(res[p]["llep"], res[p]["ep"]) and bool(res[p]["same"])
 
 
+@pytest.mark.parametrize("P,pct,nhot,params", [
+    (4, 30, 1, (1.0, 600, 1.3)),      # 2 LLAS force-assigns: one device ends above the capacity
+    (4, 60, 2, (1.25, 1500, 1.3)),    # force-assign with α > 1
+    (2, 95, 1, (2.0, 16, 1.0)),       # λ = 1 (never falls back), small m
+])
+def test_multiprocess_force_assign_and_params(L, tmp_path, P, pct, nhot, params):
+    """Plans with force-assigns and non-default α/m/λ through the whole layer."""
+    from oracle import planner as O1
+    from oracle import schedule as O2
+    alpha, m, lam = params
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29700 + P + pct),
+               LLEP_TEST_PARAMS=f"{alpha},{m},{lam}")
+    cmd = [sys.executable, os.path.join(HERE, "mp_layer_worker.py"), str(P), "tiny", str(pct), str(nhot),
+           str(tmp_path)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = [np.load(os.path.join(tmp_path, f"rank{p}.npz")) for p in range(P)]
+    sh0 = W.CONFIGS["tiny"]
+    sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, P)
+    ids_all = [W.routing_ids(sh, p, pct, nhot, 21) for p in range(P)]
+    C = O2.load_matrix(ids_all, sh.n_experts)
+    ref_plan = O1.plan(C.sum(0).tolist(), P, alpha, m, lam)
+    dp = L.parse_plan(bytes(res[0]["plan"].tobytes()))
+    assert [list(A) for A in dp.chunks] == [list(A) for A in ref_plan.chunks]
+    assert dp.force_count == ref_plan.force_count
+    if (P, pct) != (2, 95):
+        assert ref_plan.force_count > 0
+    w = LC.OracleWeights(sh.d_model, sh.d_ff, 21)
+    for p in range(P):
+        ref = LC.oracle_rank_output(sh, p, ids_all[p], W.gate_weights(sh.tokens_per_rank, sh.top_k, p, 21), 21,
+                                    weights=w)
+        mr, l2 = LC.errors(res[p]["llep"].astype(np.float64), ref)
+        assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (p, mr, l2)
+        assert bool(res[p]["same"])
+
+
+def test_q3_p1_sampled_parity(L):
+    """Qwen3-30B-A3B-shaped layer (128 experts, top-8, D=2048, H=768, 64K tokens) at P=1."""
+    sh0 = W.CONFIGS["q3"]
+    sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, 1)
+    seed = 41
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, 95, 1, seed, "cuda")
+    ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, 1, 0, 0, sh.tokens_per_rank)
+    out = ctx(x, ids, gates, w13, w2)
+    torch.cuda.synchronize()
+    ok = np.nonzero((ids_np < 12).all(1))[0]
+    rows = np.unique(np.concatenate([ok[:40], ok[-24:]]))
+    ref = LC.oracle_rank_output(sh, 0, ids_np, g_np, seed, rows=rows)
+    mr, l2 = LC.errors(_to_np(out[torch.from_numpy(rows).cuda()]), ref)
+    assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (mr, l2)
+    ctx.close()
+
+
 def test_g120_p1_sampled_parity(L):
     """BASELINE config G120 at the N=1 bench launch configuration (P=1, 32K tokens, 95 %/1):
     sampled outputs vs O3 (tokens whose experts all lie in 0..15, plus the first rows)."""

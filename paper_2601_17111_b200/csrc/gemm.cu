@@ -142,7 +142,7 @@ __device__ __forceinline__ uint32_t instr_desc() {
 }
 
 struct TileInfo {
-  int row0, row_end, nb, wslot, valid;
+  int row0, row_end, nb, wslot, small;
 };
 
 template <int TM = BM>
@@ -171,7 +171,7 @@ __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int *
   ti.row0 = g.row_base + m * TM;
   ti.row_end = g.row_base + g.n_rows;
   ti.wslot = g.wslot;
-  ti.valid = 1;
+  ti.small = g.n_rows <= kSmallGroupRows;  // its weights are streamed once: evict first from L2
   return ti;
 }
 
@@ -388,12 +388,22 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map, uint32_t leader_bar,
-                                                 int c0, int c1) {
+                                                 int c0, int c1, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar), "l"(policy)
       : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                             uint32_t idesc, uint32_t accumulate) {
@@ -468,6 +478,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
   if (warp == 0) {
     if (lane == 0) {
       // ---------------------------------------------------------------- TMA producer (both CTAs)
+      // L2 policy: a small group's weights are read by one m-block only (evict first) so they do
+      // not push the large groups' re-used weights and activation tiles out of L2
+      const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_normal();
+      const uint64_t pol_act = l2_policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < total_tiles; t += n_pairs) {
@@ -480,8 +494,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
           const uint32_t fl = smem_u32(full + stage);
           if (leader) mbar_expect_tx(fl, 2 * C::STAGE);
           const uint32_t fb = mapa_shared(fl, 0);
-          tma_load_2d_pair(smem_u32(sA + stage * C::A_BYTES), &p.tmA, fb, kb * BK, ti.row0 + (int)crank * BM);
-          tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES), wm, fb, kb * BK, brow);
+          tma_load_2d_pair(smem_u32(sA + stage * C::A_BYTES), &p.tmA, fb, kb * BK,
+                           ti.row0 + (int)crank * BM, pol_act);
+          tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES), wm, fb, kb * BK, brow,
+                           ti.small ? pol_first : pol_last);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;

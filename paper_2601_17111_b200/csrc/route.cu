@@ -202,9 +202,10 @@ __global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_kernel(DispatchA
 
 // ------------------------------------------------------------------------------ a10: combine
 // One warp per token: out[t] = Σ_{k=0..K-1} Y[dst(t,k)] in slot order, fp32 accumulation,
-// one bf16 rounding (reverse All-to-All + reverse sort + sum over K).
+// one bf16 rounding (reverse All-to-All + reverse sort + sum over K).  The K source
+// rows (local or peer-mapped) are resolved once per token; each lane then streams two 16-byte
+// vectors of every source row per iteration (2K loads in flight per lane).
 constexpr int kCombineWarps = 8;
-constexpr int kCombineKMax = 8;
 
 __device__ __forceinline__ void acc_bf16x8(float *acc, const int4 &v) {
   const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
@@ -215,7 +216,15 @@ __device__ __forceinline__ void acc_bf16x8(float *acc, const int4 &v) {
     acc[2 * i + 1] += f.y;
   }
 }
+__device__ __forceinline__ int4 pack_bf16x8(const float *acc) {
+  int4 o;
+  __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(acc[2 * u], acc[2 * u + 1]);
+  return o;
+}
 
+template <int KM>  // compile-time bound on K (K <= KM)
 __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * kCombineWarps + (threadIdx.x >> 5);
@@ -227,31 +236,38 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
     row = a.slot_dst[2 * (t * K + lane) + 1];
   }
   const int nv = a.D / 8;
+  const int4 *src[KM];
+#pragma unroll
+  for (int k = 0; k < KM; ++k) {
+    const int d = __shfl_sync(0xffffffffu, dev, k & 31);
+    const int r = __shfl_sync(0xffffffffu, row, k & 31);
+    src[k] = (k < K && d >= 0) ? reinterpret_cast<const int4 *>(a.peer_y[d]) + (int64_t)r * nv : nullptr;
+  }
   int4 *dst = reinterpret_cast<int4 *>(a.out) + t * nv;
-  for (int i = lane; i < nv; i += 32) {
-    float acc[8];
+  for (int i = lane; i < nv; i += 64) {
+    const bool two = i + 32 < nv;
+    int4 v0[KM], v1[KM];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] = 0.f;
-    for (int k0 = 0; k0 < K; k0 += kCombineKMax) {
-      int4 v[kCombineKMax];
-#pragma unroll
-      for (int kk = 0; kk < kCombineKMax; ++kk) {
-        const int k = k0 + kk;
-        const int d = __shfl_sync(0xffffffffu, dev, k & 31);
-        const int r = __shfl_sync(0xffffffffu, row, k & 31);
-        v[kk] = make_int4(0, 0, 0, 0);
-        if (k < K && d >= 0)
-          v[kk] = *(reinterpret_cast<const int4 *>(a.peer_y[d]) + (int64_t)r * nv + i);
+    for (int k = 0; k < KM; ++k) {
+      v0[k] = make_int4(0, 0, 0, 0);
+      v1[k] = make_int4(0, 0, 0, 0);
+      if (src[k]) {
+        v0[k] = __ldcs(src[k] + i);
+        if (two) v1[k] = __ldcs(src[k] + i + 32);
       }
-#pragma unroll
-      for (int kk = 0; kk < kCombineKMax; ++kk)
-        if (k0 + kk < K) acc_bf16x8(acc, v[kk]);
     }
-    int4 o;
-    __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+    float acc0[8], acc1[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(acc[2 * u], acc[2 * u + 1]);
-    dst[i] = o;
+    for (int u = 0; u < 8; ++u) acc0[u] = acc1[u] = 0.f;
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {   // slot order k = 0..K-1
+      if (k < K) {
+        acc_bf16x8(acc0, v0[k]);
+        acc_bf16x8(acc1, v1[k]);
+      }
+    }
+    __stcs(dst + i, pack_bf16x8(acc0));
+    if (two) __stcs(dst + i + 32, pack_bf16x8(acc1));
   }
 }
 
@@ -306,8 +322,12 @@ cudaError_t launch_dispatch(const DispatchArgs &a, cudaStream_t s) {
 
 cudaError_t launch_combine(const CombineArgs &a, cudaStream_t s) {
   if (a.B == 0) return cudaSuccess;
-  const int64_t blocks = (a.B + kCombineWarps - 1) / kCombineWarps;
-  combine_kernel<<<(unsigned)blocks, kCombineWarps * 32, 0, s>>>(a);
+  const unsigned blocks = (unsigned)((a.B + kCombineWarps - 1) / kCombineWarps);
+  if (a.K <= 2) combine_kernel<2><<<blocks, kCombineWarps * 32, 0, s>>>(a);
+  else if (a.K <= 4) combine_kernel<4><<<blocks, kCombineWarps * 32, 0, s>>>(a);
+  else if (a.K <= 8) combine_kernel<8><<<blocks, kCombineWarps * 32, 0, s>>>(a);
+  else if (a.K <= 16) combine_kernel<16><<<blocks, kCombineWarps * 32, 0, s>>>(a);
+  else combine_kernel<32><<<blocks, kCombineWarps * 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -16,7 +16,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libllep.so")
+LIB_PATH = os.environ.get("LLEP_LIB") or os.path.join(_PKG, "libllep.so")  # LLEP_LIB: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2601_17111_b200.build`")

@@ -2,7 +2,7 @@
 # A/B of grouped-GEMM variants at fixed (base) clocks: duration + tensor-pipe activity per launch.
 # usage: tools/ab_ncu.sh <layout> [variants] [iters]
 L=${1:-g120p1}; V=${2:-cta1,cta2}; IT=${3:-1}
-ncu --clock-control base --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum \
+ncu --clock-control base --metrics gpu__time_duration.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum \
     -k regex:grouped_gemm --csv python tools/gemm_bench.py --layout $L --iters $IT --variants $V 2>/dev/null \
   | python -c "
 import csv,sys

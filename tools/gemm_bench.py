@@ -48,7 +48,8 @@ def main():
     D, H = args.D, args.H
     sizes = layout(args.layout)
     E = len(sizes)
-    groups, rows = groups_of(sizes, E, 256)
+    groups1, rows1 = groups_of(sizes, E, 128)
+    groups2, rows = groups_of(sizes, E, 256)
     x = torch.randn(rows, D, device="cuda").to(torch.bfloat16)
     w13 = (torch.randn(E, 2 * H, D, device="cuda") / D ** 0.5).to(torch.bfloat16)
     w2 = (torch.randn(E, D, H, device="cuda") / H ** 0.5).to(torch.bfloat16)
@@ -63,6 +64,7 @@ def main():
         else:
             os.environ.pop("LLEP_GEMM_GROUP_ORDER", None)
         pair = variant == "cta2"
+        groups = groups2 if pair else groups1
         for mode in (0, 1):
             ts = []
             for it in range(args.iters + 3):

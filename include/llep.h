@@ -147,6 +147,12 @@ llep_status llep_context_reserve(llep_context *ctx, int64_t rows, int32_t foreig
 /* Bytes the context currently holds on the device (arena + scratch). */
 int64_t llep_context_device_bytes(const llep_context *ctx);
 
+/* Per-GPU memory cap for the context's device allocations (0 = none).  A llep_context_reserve that
+ * would take the context above `bytes` fails with LLEP_ERR_NOMEM and leaves the arena unchanged:
+ * the "tight per-GPU memory cap" of the Qwen3-shaped benchmark (BASELINE.json), under which standard
+ * EP's hot device cannot hold its receive rows while LLEP's capacity-bounded plan fits (§4). */
+llep_status llep_context_set_memory_cap(llep_context *ctx, int64_t bytes);
+
 /* Needs of one plan, identical on every rank (the plan is replicated and deterministic). */
 typedef struct {
   int64_t rows_needed;     /* max_d padded receive rows of device d (groups 128-row aligned)  */

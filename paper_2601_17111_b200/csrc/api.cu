@@ -182,6 +182,7 @@ using namespace llep;
 struct llep_context {
   int32_t N, K, D, H, P, M, rank, device, num_sms;
   int32_t row_align = 256;  // 256: 2-CTA GEMM tiles; 128: 1-CTA tiles (LLEP_ROW_ALIGN=128)
+  int64_t mem_cap = 0;      // 0: no cap on scratch + arena + activations
   int64_t max_tokens;
   // rank-local scratch
   int32_t *tile_cnt = nullptr, *tile_off = nullptr, *cnt = nullptr, *local_rank = nullptr;
@@ -192,8 +193,9 @@ struct llep_context {
   int32_t *sched = nullptr;
   int64_t sched_cap = 0;
   LayoutSummary *summary = nullptr;
-  LayoutSummary *summary_host = nullptr;  // pinned
-  int32_t *err_host = nullptr;            // pinned
+  LayoutSummary *summary_host = nullptr;  // mapped pinned (written by mirror_kernel)
+  int32_t *err_host = nullptr;            // mapped pinned
+  uint8_t *plan_mirror = nullptr;         // mapped pinned, plan blob bytes
   uint16_t *act = nullptr;                // A [arena_rows, H]
   size_t scratch_bytes = 0;
   // symmetric arena
@@ -285,6 +287,17 @@ static llep_status upload_peer_ptrs(llep_context *c) {
 static llep_status alloc_arena(llep_context *c, int64_t rows, int32_t foreign) {
   rows = std::max<int64_t>(rows, kRowAlign);
   foreign = std::max(foreign, 1);
+  if (c->mem_cap > 0) {
+    llep_context probe_sizes;  // offsets only
+    probe_sizes.N = c->N; probe_sizes.D = c->D; probe_sizes.H = c->H; probe_sizes.P = c->P;
+    layout_offsets(&probe_sizes, rows, foreign);
+    const int64_t need = (int64_t)(probe_sizes.arena_bytes + c->scratch_bytes + (size_t)rows * c->H * 2);
+    if (need > c->mem_cap) {
+      set_error("memory cap: the plan needs %.2f GB on this device (arena + activations + scratch), "
+                "cap %.2f GB", need / 1e9, c->mem_cap / 1e9);
+      return LLEP_ERR_NOMEM;
+    }
+  }
   close_peers(c);
   if (c->arena) cudaFree(c->arena);
   if (c->act) cudaFree(c->act);
@@ -405,8 +418,9 @@ llep_status llep_context_create(const llep_shape *s, int32_t rank, int32_t devic
   if (!e) e = A(&c->summary, sizeof(LayoutSummary));
   if (!e) e = A(&c->d_ptrs, sizeof(void *) * 4 * P);
   if (!e) e = cudaMemset(c->err, 0, sizeof(int32_t) * 4);
-  if (!e) e = cudaMallocHost(&c->summary_host, sizeof(LayoutSummary));
-  if (!e) e = cudaMallocHost(&c->err_host, sizeof(int32_t) * 4);
+  if (!e) e = cudaHostAlloc(&c->summary_host, sizeof(LayoutSummary), cudaHostAllocMapped);
+  if (!e) e = cudaHostAlloc(&c->err_host, sizeof(int32_t) * 4, cudaHostAllocMapped);
+  if (!e) e = cudaHostAlloc(&c->plan_mirror, plan_layout(c->N, c->P).bytes, cudaHostAllocMapped);
   if (!e) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
   if (!e) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   if (!e) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
@@ -437,6 +451,7 @@ void llep_context_destroy(llep_context *c) {
     if (p) cudaFree(p);
   if (c->summary_host) cudaFreeHost(c->summary_host);
   if (c->err_host) cudaFreeHost(c->err_host);
+  if (c->plan_mirror) cudaFreeHost(c->plan_mirror);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -485,6 +500,12 @@ llep_status llep_context_reserve(llep_context *c, int64_t rows, int32_t foreign)
   LLEP_CUDA(cudaSetDevice(c->device));
   LLEP_CUDA(cudaDeviceSynchronize());
   return alloc_arena(c, std::max(rows, c->arena_rows), std::max(foreign, c->arena_foreign));
+}
+
+llep_status llep_context_set_memory_cap(llep_context *c, int64_t bytes) {
+  if (!c || bytes < 0) return invalid("null context or negative cap");
+  c->mem_cap = bytes;
+  return LLEP_OK;
 }
 
 int64_t llep_context_device_bytes(const llep_context *c) {
@@ -543,11 +564,15 @@ static llep_status run_layout(llep_context *c, const void *plan, cudaStream_t s)
 // one host synchronisation: plan blob + layout summary + error flags
 static llep_status read_back(llep_context *c, const void *plan, cudaStream_t s) {
   const size_t pb = plan_layout(c->N, c->P).bytes;
-  c->plan_host.resize(pb);
-  LLEP_CUDA(cudaMemcpyAsync(c->plan_host.data(), plan, pb, cudaMemcpyDeviceToHost, s));
-  LLEP_CUDA(cudaMemcpyAsync(c->summary_host, c->summary, sizeof(LayoutSummary), cudaMemcpyDeviceToHost, s));
-  LLEP_CUDA(cudaMemcpyAsync(c->err_host, c->err, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, s));
+  void *dp = nullptr, *ds = nullptr, *de = nullptr;
+  LLEP_CUDA(cudaHostGetDevicePointer(&dp, c->plan_mirror, 0));
+  LLEP_CUDA(cudaHostGetDevicePointer(&ds, c->summary_host, 0));
+  LLEP_CUDA(cudaHostGetDevicePointer(&de, c->err_host, 0));
+  LLEP_CUDA(launch_mirror(plan, pb, c->summary, sizeof(LayoutSummary), c->err, dp, ds,
+                          reinterpret_cast<int32_t *>(de), s));
+  ++c->launches;
   LLEP_CUDA(cudaStreamSynchronize(s));
+  c->plan_host.assign(c->plan_mirror, c->plan_mirror + pb);
   c->plan_dev_cached = plan;
   if (c->err_host[0]) {
     cudaMemsetAsync(c->err, 0, sizeof(int32_t) * 4, s);

@@ -119,6 +119,9 @@ cudaError_t launch_planner(const int32_t *load_matrix, int32_t N, int32_t P, dou
                            int64_t min_chunk, double lambda, int32_t force_ep, void *plan,
                            cudaStream_t s);
 cudaError_t launch_layout(const LayoutArgs &a, cudaStream_t s);
+cudaError_t launch_mirror(const void *plan, size_t plan_bytes, const void *summary, size_t sum_bytes,
+                          const int32_t *err, void *host_plan, void *host_sum, int32_t *host_err,
+                          cudaStream_t s);
 
 struct DispatchArgs {
   const uint16_t *x;        // [B, D]

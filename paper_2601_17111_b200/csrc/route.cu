@@ -271,7 +271,30 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
   }
 }
 
+// ----------------------------------------------------------------------- host read-back
+// Copies the plan blob, the layout summary and the error flags into mapped pinned host memory
+// with plain stores (zero-copy), so the one host synchronisation of the layer never queues
+// behind bulk copies that other streams have pending on the copy engines.
+__global__ void mirror_kernel(const uint32_t *__restrict__ plan, int n_plan_words,
+                              const uint32_t *__restrict__ summary, int n_sum_words,
+                              const int32_t *__restrict__ err, uint32_t *__restrict__ host_plan,
+                              uint32_t *__restrict__ host_sum, int32_t *__restrict__ host_err) {
+  for (int i = threadIdx.x; i < n_plan_words; i += blockDim.x) host_plan[i] = plan[i];
+  for (int i = threadIdx.x; i < n_sum_words; i += blockDim.x) host_sum[i] = summary[i];
+  if (threadIdx.x < 4) host_err[threadIdx.x] = err[threadIdx.x];
+}
+
 }  // namespace
+
+cudaError_t launch_mirror(const void *plan, size_t plan_bytes, const void *summary, size_t sum_bytes,
+                          const int32_t *err, void *host_plan, void *host_sum, int32_t *host_err,
+                          cudaStream_t s) {
+  mirror_kernel<<<1, 256, 0, s>>>(reinterpret_cast<const uint32_t *>(plan), (int)(plan_bytes / 4),
+                                  reinterpret_cast<const uint32_t *>(summary), (int)(sum_bytes / 4), err,
+                                  reinterpret_cast<uint32_t *>(host_plan), reinterpret_cast<uint32_t *>(host_sum),
+                                  host_err);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_tile_count(const int32_t *ids, int64_t n_slots, int32_t N, int32_t *tile_cnt,
                               int32_t *err, cudaStream_t s) {

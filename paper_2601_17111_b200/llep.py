@@ -68,6 +68,7 @@ _SIGS = {
     "llep_context_open_peers": (ctypes.c_int, [_vp, _vp, _i32]),
     "llep_context_reserve": (ctypes.c_int, [_vp, _i64, _i32]),
     "llep_context_device_bytes": (_i64, [_vp]),
+    "llep_context_set_memory_cap": (ctypes.c_int, [_vp, _i64]),
     "llep_prepare": (ctypes.c_int, [_vp, _vp, _i64, ctypes.POINTER(Params), _i32, _vp,
                                     ctypes.POINTER(Requirements), _vp]),
     "llep_moe_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
@@ -225,6 +226,9 @@ class Context:
         _check(_lib.llep_context_stats(self._h, ctypes.byref(st), int(reset)))
         return {"ms": dict(zip(PHASES, list(st.ms))), "calls": int(st.calls),
                 "kernel_launches": int(st.kernel_launches), "gemm_rows": int(st.gemm_rows)}
+
+    def set_memory_cap(self, nbytes: int) -> None:
+        _check(_lib.llep_context_set_memory_cap(self._h, int(nbytes)))
 
     def device_bytes(self) -> int:
         return int(_lib.llep_context_device_bytes(self._h))

@@ -79,8 +79,8 @@ def _ref_gemm(mode, a, w, groups, nout, gate):
 def test_grouped_gemm(L, mode, kdim, nout, pair):
     g = torch.Generator(device="cuda").manual_seed(kdim * 7 + nout)
     E = 3
-    sizes = [1, 300, 0, 129, 128, 77, 600]
-    ra = 256 if pair else 128
+    sizes = [1, 300, 0, 129, 128, 77, 600, 256, 385]
+    ra = 256 if pair else 128  # 2-CTA pair tiles are 256 rows: group bases 256-aligned
     groups, rb = [], 0
     for i, n in enumerate(sizes):
         if n == 0:

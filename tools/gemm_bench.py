@@ -49,7 +49,7 @@ def main():
     sizes = layout(args.layout)
     E = len(sizes)
     groups1, rows1 = groups_of(sizes, E, 128)
-    groups2, rows = groups_of(sizes, E, 256)
+    groups2, rows = groups_of(sizes, E, int(os.environ.get("GB_RA", "256")))
     x = torch.randn(rows, D, device="cuda").to(torch.bfloat16)
     w13 = (torch.randn(E, 2 * H, D, device="cuda") / D ** 0.5).to(torch.bfloat16)
     w2 = (torch.randn(E, D, H, device="cuda") / H ** 0.5).to(torch.bfloat16)

@@ -139,10 +139,16 @@ void llep_context_destroy(llep_context *ctx);
 llep_status llep_context_ipc_handle(llep_context *ctx, void *handle64);
 llep_status llep_context_open_peers(llep_context *ctx, const void *handles, int32_t n);
 
-/* Grow the arena so every rank can receive `rows` padded rows and `foreign` imported experts.
- * Collective: all ranks must call it with the same arguments, then redo the handle exchange.
- * The numbers come from llep_requirements (identical on every rank). */
-llep_status llep_context_reserve(llep_context *ctx, int64_t rows, int32_t foreign);
+/* Grow the arena so every rank can receive `rows` padded rows, `foreign` imported experts and (with
+ * the backward pass enabled) `grad_slots` returned weight-gradient partials.  Collective: all ranks
+ * must call it with the same arguments, then redo the handle exchange.  The numbers come from
+ * llep_requirements (identical on every rank). */
+llep_status llep_context_reserve(llep_context *ctx, int64_t rows, int32_t foreign, int32_t grad_slots);
+
+/* Enable the backward pass (row f1): the arena gains the upstream-gradient rows and the slots that
+ * receive spilled experts' weight-gradient partials, plus rank-local buffers.  Collective
+ * like llep_context_reserve (re-exchange the IPC handles afterwards for P > 1). */
+llep_status llep_context_enable_backward(llep_context *ctx);
 
 /* Bytes the context currently holds on the device (arena + scratch). */
 int64_t llep_context_device_bytes(const llep_context *ctx);
@@ -161,6 +167,7 @@ typedef struct {
   int64_t my_rows;         /* g_a[rank]                                                         */
   int32_t my_groups;       /* expert groups this rank computes (native with rows + foreign)    */
   int32_t fallback_ep, force_count, n_transfers;
+  int32_t grad_slots_needed; /* backward: max_d weight-gradient partials returned to device d   */
 } llep_requirements;
 
 /* ------------------------------------------------------------------ the hot path
@@ -197,6 +204,24 @@ llep_status llep_prepare(llep_context *ctx, const int32_t *topk_ids, int64_t n_t
 llep_status llep_moe_forward(llep_context *ctx, const uint16_t *x, const int32_t *topk_ids,
                              const float *topk_w, int64_t n_tokens, const uint16_t *w13,
                              const uint16_t *w2, const void *plan, uint16_t *out, void *stream);
+
+/* llep_moe_backward -- the backward pass of the layer (row f1) under the plan of
+ * llep_prepare for these topk_ids, recomputing the forward internals (nothing is kept from a
+ * forward call), for the loss L with dL/dout = dout:
+ *   dispatch x and dout rows + gates (a6) ‖ weight pushes (a7) -> barrier
+ *   GU = X·W13ᵀ (gate/up pre-activations, tcgen05)       dA0 = dO·W_down   (MN-major tcgen05 GEMM)
+ *   per row: a = silu(g)u, da = w·dA0, dg = da·u·silu'(g), du = da·silu(g), dL/dw = <a, dA0>
+ *   dW_down = dOᵀ·(w·a), dW13 = [dg|du]ᵀ·X (per expert, contraction over its rows), dX = [dg|du]·W13
+ *   replicas push the weight-gradient partials of spilled experts to the native device, which adds
+ *   them in ascending source-device order -> barrier -> combine dX rows (Σ_K, slot order)
+ *   dout     [B, D] bf16          dx [B, D] bf16         dgates [B, K] fp32 (dL/dtopk_w)
+ *   dw13     [M, 2H, D] fp32 (dL/dW_gate rows 0..H-1, dL/dW_up rows H..2H-1)   dw2 [M, D, H] fp32
+ * Requires llep_context_enable_backward and the arena of llep_requirements.fits.
+ * Errors: INVALID, PLAN, CUDA, COMM. */
+llep_status llep_moe_backward(llep_context *ctx, const uint16_t *x, const int32_t *topk_ids,
+                              const float *topk_w, const uint16_t *dout, int64_t n_tokens,
+                              const uint16_t *w13, const uint16_t *w2, const void *plan, uint16_t *dx,
+                              float *dgates, float *dw13, float *dw2, void *stream);
 
 /* ------------------------------------------------------------------ measurement
  * Per-phase device time, from CUDA events recorded on the caller's stream at the phase
@@ -259,6 +284,17 @@ llep_status llep_grouped_gemm(int32_t mode, const uint16_t *a, int64_t rows, int
                               const uint16_t *w, int32_t n_weights, int32_t nout,
                               const int32_t *groups, int32_t n_groups, const float *gate,
                               uint16_t *out, void *stream);
+
+/* Standalone backward-pass GEMMs (row f1; kernel tests / micro-bench), MN-major tcgen05 operands:
+ *   kind 0: out[r, 0:nout] = a[r, 0:kdim] · w[e][kdim, nout] for r in group rows (bf16 out [rows, nout]);
+ *           a [rows, kdim] bf16, w [E, kdim, nout] bf16 row-major (e.g. W_down [D][H], W13 [2H][D])
+ *   kind 1: out[e][mdim, nout] = Σ_{r in group} a[r, 0:mdim] ⊗ b[r, 0:nout]  (fp32 out [E, mdim, nout]);
+ *           a [rows, mdim], b [rows, nout] bf16; rows past a group's end up to the next multiple of
+ *           256 must be zero in a and b (the contraction runs over whole 256-row blocks)
+ * groups: HOST int32 [G*4] = (expert / output slot, row_base, n_rows, 0), row_base % 256 == 0. */
+llep_status llep_gemm_bwd(int32_t kind, const uint16_t *a, const uint16_t *w_or_b, int64_t rows,
+                          int32_t kdim_or_mdim, int32_t nout, int32_t n_weights, const int32_t *groups,
+                          int32_t n_groups, void *out, void *stream);
 
 #ifdef __cplusplus
 }

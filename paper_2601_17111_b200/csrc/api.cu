@@ -204,10 +204,16 @@ struct llep_context {
   int64_t arena_rows = 0;
   int32_t arena_foreign = 0;
   size_t off_flags = 0, off_lm = 0, off_x = 0, off_g = 0, off_w13 = 0, off_w2 = 0;
+  // backward (row f1): arena regions O [R, D] bf16 + returned weight-gradient slots, local buffers
+  bool backward = false;
+  int32_t arena_grad = 0;
+  size_t off_o = 0, off_grad = 0;
+  uint16_t *gu = nullptr, *da0 = nullptr, *aw = nullptr, *dgu = nullptr;
+  float *stage13 = nullptr, *stage2 = nullptr;
   uint8_t *peer_base[kMaxWorld] = {};
   bool peer_opened[kMaxWorld] = {};
   bool peers_ready = false;
-  void **d_ptrs = nullptr;  // device: flags[P], lm[P], x[P], g[P]
+  void **d_ptrs = nullptr;  // device: flags[P], lm[P], x[P], g[P], o[P], grad[P]
   uint32_t epoch = 0;
   // host copy of the last prepared plan
   std::vector<uint8_t> plan_host;
@@ -259,7 +265,18 @@ static void layout_offsets(llep_context *c, int64_t rows, int32_t foreign) {
   off = (off + 1023) & ~size_t(1023);
   c->off_w2 = off;
   off += (size_t)foreign * c->D * c->H * 2;
+  off = (off + 1023) & ~size_t(1023);
+  c->off_o = off;
+  if (c->backward) off += (size_t)rows * c->D * 2;
+  off = (off + 1023) & ~size_t(1023);
+  c->off_grad = off;
+  if (c->backward) off += (size_t)c->arena_grad * 3 * c->H * c->D * 4;
   c->arena_bytes = (off + 4095) & ~size_t(4095);
+}
+
+static size_t bwd_local_bytes(const llep_context *c, int64_t rows, int32_t foreign) {
+  if (!c->backward) return 0;
+  return (size_t)rows * c->H * 2 * 6 + (size_t)foreign * 3 * c->H * c->D * 4;
 }
 
 static void close_peers(llep_context *c) {
@@ -272,15 +289,17 @@ static void close_peers(llep_context *c) {
 }
 
 static llep_status upload_peer_ptrs(llep_context *c) {
-  std::vector<void *> h(4 * c->P);
+  std::vector<void *> h(6 * c->P);
   for (int q = 0; q < c->P; ++q) {
     uint8_t *b = c->peer_base[q];
     h[q] = b + c->off_flags;
     h[c->P + q] = b + c->off_lm;
     h[2 * c->P + q] = b + c->off_x;
     h[3 * c->P + q] = b + c->off_g;
+    h[4 * c->P + q] = b + c->off_o;
+    h[5 * c->P + q] = b + c->off_grad;
   }
-  LLEP_CUDA(cudaMemcpy(c->d_ptrs, h.data(), sizeof(void *) * 4 * c->P, cudaMemcpyHostToDevice));
+  LLEP_CUDA(cudaMemcpy(c->d_ptrs, h.data(), sizeof(void *) * 6 * c->P, cudaMemcpyHostToDevice));
   return LLEP_OK;
 }
 
@@ -291,7 +310,11 @@ static llep_status alloc_arena(llep_context *c, int64_t rows, int32_t foreign) {
     llep_context probe_sizes;  // offsets only
     probe_sizes.N = c->N; probe_sizes.D = c->D; probe_sizes.H = c->H; probe_sizes.P = c->P;
     layout_offsets(&probe_sizes, rows, foreign);
-    const int64_t need = (int64_t)(probe_sizes.arena_bytes + c->scratch_bytes + (size_t)rows * c->H * 2);
+    probe_sizes.backward = c->backward;
+    probe_sizes.arena_grad = c->arena_grad;
+    layout_offsets(&probe_sizes, rows, foreign);
+    const int64_t need = (int64_t)(probe_sizes.arena_bytes + c->scratch_bytes + (size_t)rows * c->H * 2 +
+                                   bwd_local_bytes(c, rows, foreign));
     if (need > c->mem_cap) {
       set_error("memory cap: the plan needs %.2f GB on this device (arena + activations + scratch), "
                 "cap %.2f GB", need / 1e9, c->mem_cap / 1e9);
@@ -301,12 +324,25 @@ static llep_status alloc_arena(llep_context *c, int64_t rows, int32_t foreign) {
   close_peers(c);
   if (c->arena) cudaFree(c->arena);
   if (c->act) cudaFree(c->act);
+  void *bufs[] = {c->gu, c->da0, c->aw, c->dgu, c->stage13, c->stage2};
+  for (void *b : bufs)
+    if (b) cudaFree(b);
+  c->gu = c->da0 = c->aw = c->dgu = nullptr;
+  c->stage13 = c->stage2 = nullptr;
   c->arena = nullptr;
   c->act = nullptr;
   layout_offsets(c, rows, foreign);
   LLEP_CUDA(cudaMalloc(&c->arena, c->arena_bytes));
   LLEP_CUDA(cudaMemset(c->arena, 0, c->off_x));  // flags + load matrix
   LLEP_CUDA(cudaMalloc(&c->act, (size_t)rows * c->H * 2));
+  if (c->backward) {
+    LLEP_CUDA(cudaMalloc(&c->gu, (size_t)rows * 2 * c->H * 2));
+    LLEP_CUDA(cudaMalloc(&c->da0, (size_t)rows * c->H * 2));
+    LLEP_CUDA(cudaMalloc(&c->aw, (size_t)rows * c->H * 2));
+    LLEP_CUDA(cudaMalloc(&c->dgu, (size_t)rows * 2 * c->H * 2));
+    LLEP_CUDA(cudaMalloc(&c->stage13, (size_t)foreign * 2 * c->H * c->D * 4));
+    LLEP_CUDA(cudaMalloc(&c->stage2, (size_t)foreign * c->H * c->D * 4));
+  }
   c->arena_rows = rows;
   c->arena_foreign = foreign;
   c->peer_base[c->rank] = c->arena;
@@ -416,7 +452,7 @@ llep_status llep_context_create(const llep_shape *s, int32_t rank, int32_t devic
   c->sched_cap = ((int64_t)P * slots + kRowAlign - 1) / kRowAlign + kMaxGroups;
   if (!e) e = A(&c->sched, sizeof(int32_t) * c->sched_cap);
   if (!e) e = A(&c->summary, sizeof(LayoutSummary));
-  if (!e) e = A(&c->d_ptrs, sizeof(void *) * 4 * P);
+  if (!e) e = A(&c->d_ptrs, sizeof(void *) * 6 * P);
   if (!e) e = cudaMemset(c->err, 0, sizeof(int32_t) * 4);
   if (!e) e = cudaHostAlloc(&c->summary_host, sizeof(LayoutSummary), cudaHostAllocMapped);
   if (!e) e = cudaHostAlloc(&c->err_host, sizeof(int32_t) * 4, cudaHostAllocMapped);
@@ -446,7 +482,8 @@ void llep_context_destroy(llep_context *c) {
   close_peers(c);
   void *ptrs[] = {c->tile_cnt, c->tile_off, c->cnt, c->local_rank, c->slot_dst, c->err,
                   c->lm_local, c->rows_on, c->chunk_row, c->foreign_slot, c->dev_padded,
-                  c->dev_foreign, c->groups, c->sched, c->summary, c->d_ptrs, c->act, c->arena};
+                  c->dev_foreign, c->groups, c->sched, c->summary, c->d_ptrs, c->act, c->arena,
+                  c->gu, c->da0, c->aw, c->dgu, c->stage13, c->stage2};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->summary_host) cudaFreeHost(c->summary_host);
@@ -494,12 +531,28 @@ llep_status llep_context_open_peers(llep_context *c, const void *handles, int32_
   return upload_peer_ptrs(c);
 }
 
-llep_status llep_context_reserve(llep_context *c, int64_t rows, int32_t foreign) {
+llep_status llep_context_reserve(llep_context *c, int64_t rows, int32_t foreign, int32_t grad_slots) {
   if (!c) return invalid("null context");
-  if (rows <= c->arena_rows && foreign <= c->arena_foreign && c->peers_ready) return LLEP_OK;
+  if (rows <= c->arena_rows && foreign <= c->arena_foreign && grad_slots <= c->arena_grad && c->peers_ready)
+    return LLEP_OK;
   LLEP_CUDA(cudaSetDevice(c->device));
   LLEP_CUDA(cudaDeviceSynchronize());
-  return alloc_arena(c, std::max(rows, c->arena_rows), std::max(foreign, c->arena_foreign));
+  const int32_t old_grad = c->arena_grad;
+  c->arena_grad = std::max(grad_slots, c->arena_grad);
+  llep_status st = alloc_arena(c, std::max(rows, c->arena_rows), std::max(foreign, c->arena_foreign));
+  if (st != LLEP_OK) c->arena_grad = old_grad;
+  return st;
+}
+
+llep_status llep_context_enable_backward(llep_context *c) {
+  if (!c) return invalid("null context");
+  if (c->row_align != 256) return invalid("the backward pass needs the 256-row (2-CTA) group layout");
+  if (c->backward) return LLEP_OK;
+  LLEP_CUDA(cudaSetDevice(c->device));
+  LLEP_CUDA(cudaDeviceSynchronize());
+  c->backward = true;
+  // regions change: collective like llep_context_reserve (re-exchange the IPC handles for P > 1)
+  return alloc_arena(c, c->arena_rows, c->arena_foreign);
 }
 
 llep_status llep_context_set_memory_cap(llep_context *c, int64_t bytes) {
@@ -526,11 +579,27 @@ static llep_status barrier(llep_context *c, cudaStream_t s) {
   return LLEP_OK;
 }
 
+// max over devices of the weight-gradient partials returned to it (𝒲 entries with src = device)
+static int32_t grad_slots_needed(const llep_context *c) {
+  const PlanLayout L = plan_layout(c->N, c->P);
+  const uint8_t *rep = c->plan_host.data() + L.off_replica;
+  int32_t mx = 0;
+  for (int n = 0; n < c->P; ++n) {
+    int32_t k = 0;
+    for (int e = n * c->M; e < (n + 1) * c->M; ++e)
+      for (int d = 0; d < c->P; ++d) k += rep[(size_t)e * c->P + d];
+    mx = std::max(mx, k);
+  }
+  return mx;
+}
+
 static void fill_req(llep_context *c, llep_requirements *req) {
   const LayoutSummary &s = *c->summary_host;
   req->rows_needed = s.rows_needed;
   req->foreign_needed = s.foreign_needed;
-  req->fits = (s.rows_needed <= c->arena_rows && s.foreign_needed <= c->arena_foreign) ? 1 : 0;
+  req->grad_slots_needed = c->backward ? grad_slots_needed(c) : 0;
+  req->fits = (s.rows_needed <= c->arena_rows && s.foreign_needed <= c->arena_foreign &&
+               req->grad_slots_needed <= c->arena_grad) ? 1 : 0;
   req->my_rows = s.my_rows;
   req->my_groups = s.my_groups;
   req->fallback_ep = s.fallback_ep;
@@ -636,6 +705,40 @@ llep_status llep_prepare(llep_context *c, const int32_t *ids, int64_t B, const l
   return LLEP_OK;
 }
 
+// a7: for every 𝒲 entry (e, rank -> d) copy W13_e and W2_e into foreign slot f of device d
+// (f = position of e among d's foreign experts, ascending id) on the side stream (copy engines).
+static llep_status push_weights(llep_context *c, const uint16_t *w13, const uint16_t *w2, cudaStream_t s,
+                                bool *any_copy) {
+  const int N = c->N, P = c->P, M = c->M, D = c->D, H = c->H;
+  const PlanLayout L = plan_layout(N, P);
+  const uint8_t *replica = c->plan_host.data() + L.off_replica;
+  const size_t w13_bytes = (size_t)2 * H * D * 2, w2_bytes = (size_t)D * H * 2;
+  *any_copy = false;
+  for (int d = 0; d < P && P > 1; ++d) {
+    if (d == c->rank) continue;
+    int f = 0;
+    for (int e = 0; e < N; ++e) {
+      if (!replica[(size_t)e * P + d]) continue;
+      if (e / M == c->rank) {
+        if (!*any_copy) {
+          LLEP_CUDA(cudaEventRecord(c->ev_fork, s));
+          LLEP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+          *any_copy = true;
+        }
+        const int el = e - c->rank * M;
+        LLEP_CUDA(cudaMemcpyAsync(c->peer_base[d] + c->off_w13 + (size_t)f * w13_bytes,
+                                  w13 + (size_t)el * 2 * H * D, w13_bytes, cudaMemcpyDeviceToDevice,
+                                  c->side));
+        LLEP_CUDA(cudaMemcpyAsync(c->peer_base[d] + c->off_w2 + (size_t)f * w2_bytes,
+                                  w2 + (size_t)el * D * H, w2_bytes, cudaMemcpyDeviceToDevice,
+                                  c->side));
+      }
+      ++f;
+    }
+  }
+  return LLEP_OK;
+}
+
 llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *ids,
                              const float *topk_w, int64_t B, const uint16_t *w13,
                              const uint16_t *w2, const void *plan, uint16_t *out, void *stream) {
@@ -656,34 +759,10 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
     return LLEP_ERR_PLAN;
   }
   const int N = c->N, P = c->P, M = c->M, D = c->D, H = c->H;
+  (void)H;
   // a7: weight migration, pushed by the native device on a side stream (copy engines)
-  const PlanLayout L = plan_layout(N, P);
-  const uint8_t *ph = c->plan_host.data();
-  const uint8_t *replica = ph + L.off_replica;
-  const size_t w13_bytes = (size_t)2 * H * D * 2, w2_bytes = (size_t)D * H * 2;
   bool any_copy = false;
-  for (int d = 0; d < P && P > 1; ++d) {
-    if (d == c->rank) continue;
-    int f = 0;
-    for (int e = 0; e < N; ++e) {
-      if (!replica[(size_t)e * P + d]) continue;
-      if (e / M == c->rank) {
-        if (!any_copy) {
-          LLEP_CUDA(cudaEventRecord(c->ev_fork, s));
-          LLEP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-          any_copy = true;
-        }
-        const int el = e - c->rank * M;
-        LLEP_CUDA(cudaMemcpyAsync(c->peer_base[d] + c->off_w13 + (size_t)f * w13_bytes,
-                                  w13 + (size_t)el * 2 * H * D, w13_bytes, cudaMemcpyDeviceToDevice,
-                                  c->side));
-        LLEP_CUDA(cudaMemcpyAsync(c->peer_base[d] + c->off_w2 + (size_t)f * w2_bytes,
-                                  w2 + (size_t)el * D * H, w2_bytes, cudaMemcpyDeviceToDevice,
-                                  c->side));
-      }
-      ++f;
-    }
-  }
+  if ((st = push_weights(c, w13, w2, s, &any_copy)) != LLEP_OK) return st;
   mark(c, 4, s);
   if (any_copy) LLEP_CUDA(cudaEventRecord(c->ev_join, c->side));
   // a6: dispatch (gather-on-send into every destination's receive rows)
@@ -704,6 +783,8 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   da.peer_x = peer_x(c);
   da.peer_g = peer_g(c);
   da.slot_dst = c->slot_dst;
+  da.x2 = nullptr;
+  da.peer_x2 = nullptr;
   LLEP_CUDA(launch_dispatch(da, s));
   c->launches += B > 0;
   if (any_copy) LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
@@ -754,12 +835,226 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   ca.K = c->K;
   ca.D = D;
   ca.out = out;
+  ca.peer_s = nullptr;
+  ca.slot_out = nullptr;
   LLEP_CUDA(launch_combine(ca, s));
   c->launches += B > 0;
   mark(c, 8, s);
   if (c->timing) {
     c->pending = true;
     c->pending_rows = sum.my_rows;
+  }
+  return LLEP_OK;
+}
+
+
+llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t *ids,
+                              const float *topk_w, const uint16_t *dout, int64_t B,
+                              const uint16_t *w13, const uint16_t *w2, const void *plan, uint16_t *dx,
+                              float *dgates, float *dw13, float *dw2, void *stream) {
+  if (!c || !plan || !w13 || !w2 || !dw13 || !dw2 ||
+      (B > 0 && (!x || !ids || !topk_w || !dout || !dx || !dgates)))
+    return invalid("null pointer");
+  if (!c->backward) return invalid("call llep_context_enable_backward first");
+  if (B != c->prepared_tokens) return invalid("n_tokens differs from the last llep_prepare");
+  cudaStream_t s = (cudaStream_t)stream;
+  llep_status st;
+  if (plan != c->plan_dev_cached) {
+    if ((st = run_layout(c, plan, s)) != LLEP_OK) return st;
+    if ((st = read_back(c, plan, s)) != LLEP_OK) return st;
+  }
+  const LayoutSummary &sum = *c->summary_host;
+  const int32_t gslots = grad_slots_needed(c);
+  if (sum.rows_needed > c->arena_rows || sum.foreign_needed > c->arena_foreign || gslots > c->arena_grad) {
+    set_error("plan needs %lld rows / %d foreign / %d gradient slots, arena holds %lld / %d / %d: call "
+              "llep_context_reserve", (long long)sum.rows_needed, sum.foreign_needed, gslots,
+              (long long)c->arena_rows, c->arena_foreign, c->arena_grad);
+    return LLEP_ERR_PLAN;
+  }
+  const int N = c->N, P = c->P, M = c->M, D = c->D, H = c->H;
+  const PlanLayout L = plan_layout(N, P);
+  const uint8_t *replica = c->plan_host.data() + L.off_replica;
+  const llep_chunk *chunks = reinterpret_cast<const llep_chunk *>(c->plan_host.data() + L.off_chunks);
+  const int32_t *n_chunks = reinterpret_cast<const int32_t *>(c->plan_host.data() + L.off_n_chunks);
+  const size_t slot13 = (size_t)2 * H * D, slot2 = (size_t)D * H, slot_all = slot13 + slot2;
+  uint16_t *X = reinterpret_cast<uint16_t *>(c->arena + c->off_x);
+  uint16_t *O = reinterpret_cast<uint16_t *>(c->arena + c->off_o);
+  float *G = reinterpret_cast<float *>(c->arena + c->off_g);
+  // a7 + a6: weights to the replicas, x and dout rows + gates to their destinations
+  bool any_copy = false;
+  if ((st = push_weights(c, w13, w2, s, &any_copy)) != LLEP_OK) return st;
+  if (any_copy) LLEP_CUDA(cudaEventRecord(c->ev_join, c->side));
+  DispatchArgs da;
+  da.x = x;
+  da.ids = ids;
+  da.w = topk_w;
+  da.local_rank = c->local_rank;
+  da.load_matrix = c->lm_local;
+  da.plan = plan;
+  da.chunk_row = c->chunk_row;
+  da.B = B;
+  da.K = c->K;
+  da.D = D;
+  da.N = N;
+  da.P = P;
+  da.rank = c->rank;
+  da.peer_x = peer_x(c);
+  da.peer_g = peer_g(c);
+  da.slot_dst = c->slot_dst;
+  da.x2 = dout;
+  da.peer_x2 = reinterpret_cast<uint16_t *const *>(c->d_ptrs + 4 * P);
+  LLEP_CUDA(launch_dispatch(da, s));
+  c->launches += B > 0;
+  if (any_copy) LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+  if ((st = barrier(c, s)) != LLEP_OK) return st;
+  const int G_ = sum.my_groups;
+  // native experts without rows here: their gradient (before returned partials) is zero
+  for (int el = 0; el < M; ++el) {
+    const int e = c->rank * M + el;
+    bool has = false;
+    for (int k = 0; k < n_chunks[e] && !has; ++k) has = chunks[(size_t)e * (P + 1) + k].device == c->rank;
+    if (!has) {
+      LLEP_CUDA(cudaMemsetAsync(dw13 + (size_t)el * slot13, 0, slot13 * 4, s));
+      LLEP_CUDA(cudaMemsetAsync(dw2 + (size_t)el * slot2, 0, slot2 * 4, s));
+    }
+  }
+  if (G_ > 0) {
+    LLEP_CUDA(launch_zero_pad(c->groups, G_, D, X, O, s));
+    ++c->launches;
+    // GU = X · W13ᵀ (raw gate / up pre-activations)
+    GemmArgs g1;
+    memset(&g1, 0, sizeof(g1));
+    g1.mode = 2;
+    g1.a = X;
+    g1.a_rows = c->arena_rows;
+    g1.kdim = D;
+    g1.w_native = w13;
+    g1.n_native = M;
+    g1.w_foreign = reinterpret_cast<const uint16_t *>(c->arena + c->off_w13);
+    g1.n_foreign = c->arena_foreign;
+    g1.nout = H;
+    g1.groups = c->groups;
+    g1.sched = c->sched;
+    g1.n_groups_host = G_;
+    g1.out = c->gu;
+    g1.num_sms = c->num_sms;
+    g1.row_align = c->row_align;
+    if ((st = run_grouped_gemm(g1, s)) != LLEP_OK) return st;
+    ++c->launches;
+    // dA0 = dO · W_down  (W_down [D][H] row-major: MN-major B)
+    BwdArgs b;
+    memset(&b, 0, sizeof(b));
+    b.kind = 0;
+    b.a = O;
+    b.b = w2;
+    b.rows = c->arena_rows;
+    b.kdim = D;
+    b.mdim = 8;
+    b.nout = H;
+    b.n_weights = M;
+    b.b_foreign = reinterpret_cast<const uint16_t *>(c->arena + c->off_w2);
+    b.n_foreign = c->arena_foreign;
+    b.groups = c->groups;
+    b.n_groups = G_;
+    b.mblk_scale = 2;
+    b.out = c->da0;
+    b.num_sms = c->num_sms;
+    if ((st = run_gemm_bwd(b, s)) != LLEP_OK) return st;
+    ++c->launches;
+    // SwiGLU backward per row; dL/dw replaces the gate in G
+    LLEP_CUDA(launch_bwd_swiglu(c->groups, G_, (int)sum.my_padded, H, c->gu, c->da0, G, c->aw, c->dgu, s));
+    ++c->launches;
+    // dW_down = dOᵀ · (w a)   and   dW13 = [dg|du]ᵀ · X   (native -> dw2/dw13, foreign -> staging)
+    BwdArgs w;
+    memset(&w, 0, sizeof(w));
+    w.kind = 1;
+    w.rows = c->arena_rows;
+    w.kdim = 8;
+    w.groups = c->groups;
+    w.n_groups = G_;
+    w.mblk_scale = 2;
+    w.num_sms = c->num_sms;
+    w.a = O;
+    w.b = c->aw;
+    w.mdim = D;
+    w.nout = H;
+    w.out = dw2;
+    w.out_foreign = c->stage2;
+    if ((st = run_gemm_bwd(w, s)) != LLEP_OK) return st;
+    w.a = c->dgu;
+    w.b = X;
+    w.mdim = 2 * H;
+    w.nout = D;
+    w.out = dw13;
+    w.out_foreign = c->stage13;
+    if ((st = run_gemm_bwd(w, s)) != LLEP_OK) return st;
+    c->launches += 2;
+    // dX = [dg|du] · W13   (W13 [2H][D] row-major: MN-major B), into X's rows (X is dead now)
+    b.a = c->dgu;
+    b.b = w13;
+    b.kdim = 2 * H;
+    b.nout = D;
+    b.b_foreign = reinterpret_cast<const uint16_t *>(c->arena + c->off_w13);
+    b.out = X;
+    if ((st = run_gemm_bwd(b, s)) != LLEP_OK) return st;
+    ++c->launches;
+  }
+  // push the weight-gradient partials of foreign experts to their native devices; the slot on
+  // device n of (e, d) is the position of (e, d) among n's 𝒲 entries ordered by (e, d)
+  bool any_push = false;
+  if (P > 1) {
+    int f = 0;
+    for (int e = 0; e < N; ++e) {
+      if (!replica[(size_t)e * P + c->rank]) continue;
+      const int n = e / M;
+      int slot = 0;
+      for (int e2 = n * M; e2 < (n + 1) * M; ++e2)
+        for (int d2 = 0; d2 < P; ++d2)
+          if (replica[(size_t)e2 * P + d2] && (e2 < e || (e2 == e && d2 < c->rank))) ++slot;
+      if (!any_push) {
+        LLEP_CUDA(cudaEventRecord(c->ev_fork, s));
+        LLEP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+        any_push = true;
+      }
+      uint8_t *dst = c->peer_base[n] + c->off_grad + (size_t)slot * slot_all * 4;
+      LLEP_CUDA(cudaMemcpyAsync(dst, c->stage13 + (size_t)f * slot13, slot13 * 4, cudaMemcpyDeviceToDevice, c->side));
+      LLEP_CUDA(cudaMemcpyAsync(dst + slot13 * 4, c->stage2 + (size_t)f * slot2, slot2 * 4,
+                                cudaMemcpyDeviceToDevice, c->side));
+      ++f;
+    }
+  }
+  if (any_push) {
+    LLEP_CUDA(cudaEventRecord(c->ev_join, c->side));
+    LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+  }
+  if ((st = barrier(c, s)) != LLEP_OK) return st;
+  // dx[t] = Σ_k dX[dst(t,k)] (slot order), dgates[t,k] = dL/dw of that row
+  CombineArgs ca;
+  ca.slot_dst = c->slot_dst;
+  ca.peer_y = peer_x(c);
+  ca.B = B;
+  ca.K = c->K;
+  ca.D = D;
+  ca.out = dx;
+  ca.peer_s = reinterpret_cast<const float *const *>(c->d_ptrs + 3 * P);
+  ca.slot_out = dgates;
+  LLEP_CUDA(launch_combine(ca, s));
+  c->launches += B > 0;
+  // native device: add the returned partials, ascending source device (slots are (e, d)-ordered)
+  if (P > 1) {
+    int slot = 0;
+    for (int e = c->rank * M; e < (c->rank + 1) * M; ++e) {
+      int cnt = 0;
+      for (int d2 = 0; d2 < P; ++d2) cnt += replica[(size_t)e * P + d2];
+      if (cnt) {
+        const int el = e - c->rank * M;
+        const float *base = reinterpret_cast<const float *>(c->arena + c->off_grad) + (size_t)slot * slot_all;
+        LLEP_CUDA(launch_grad_reduce(dw13 + (size_t)el * slot13, base, cnt, slot_all, slot13, s));
+        LLEP_CUDA(launch_grad_reduce(dw2 + (size_t)el * slot2, base + slot13, cnt, slot_all, slot2, s));
+        c->launches += 2;
+      }
+      slot += cnt;
+    }
   }
   return LLEP_OK;
 }
@@ -874,6 +1169,49 @@ llep_status llep_grouped_gemm(int32_t mode, const uint16_t *a, int64_t rows, int
   llep_status st = n_groups > 0 ? run_grouped_gemm(ga, s) : LLEP_OK;
   cudaFreeAsync(dg, s);
   cudaFreeAsync(dsched, s);
+  return st;
+}
+
+llep_status llep_gemm_bwd(int32_t kind, const uint16_t *a, const uint16_t *w_or_b, int64_t rows,
+                          int32_t kdim_or_mdim, int32_t nout, int32_t n_weights, const int32_t *groups,
+                          int32_t n_groups, void *out, void *stream) {
+  if (kind != 0 && kind != 1) return invalid("kind must be 0 or 1");
+  if (!a || !w_or_b || !groups || !out) return invalid("null pointer");
+  if (n_groups < 0 || n_groups > kMaxGroups) return invalid("n_groups out of range");
+  std::vector<Group> g(std::max(n_groups, 1));
+  int mb = 0;
+  for (int i = 0; i < n_groups; ++i) {
+    const int32_t *q = groups + 4 * i;
+    if (q[0] < 0 || q[0] >= n_weights) return invalid("group expert out of range");
+    if (q[1] % 256 || q[2] < 1 || q[1] + (int64_t)((q[2] + 255) / 256 * 256) > rows)
+      return invalid("group rows must start 256-aligned, be nonempty and fit (padded to 256)");
+    g[i] = Group{q[0], q[0], q[1], q[2], mb, {0, 0, 0}};
+    mb += (q[2] + 255) / 256;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  Group *dg = nullptr;
+  LLEP_CUDA(cudaMallocAsync(&dg, sizeof(Group) * g.size(), s));
+  LLEP_CUDA(cudaMemcpyAsync(dg, g.data(), sizeof(Group) * g.size(), cudaMemcpyHostToDevice, s));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  BwdArgs ba;
+  memset(&ba, 0, sizeof(ba));
+  ba.kind = kind;
+  ba.a = a;
+  ba.b = w_or_b;
+  ba.rows = rows;
+  ba.kdim = kind == 0 ? kdim_or_mdim : 8;
+  ba.mdim = kind == 1 ? kdim_or_mdim : 8;
+  ba.nout = nout;
+  ba.n_weights = n_weights;
+  ba.groups = dg;
+  ba.n_groups = n_groups;
+  ba.mblk_scale = 2;   // Group.mblk_start counts 256-row blocks
+  ba.out = out;
+  ba.num_sms = sms;
+  llep_status st = n_groups > 0 ? run_gemm_bwd(ba, s) : LLEP_OK;
+  cudaFreeAsync(dg, s);
   return st;
 }
 

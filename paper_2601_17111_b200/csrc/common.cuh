@@ -119,6 +119,12 @@ cudaError_t launch_planner(const int32_t *load_matrix, int32_t N, int32_t P, dou
                            int64_t min_chunk, double lambda, int32_t force_ep, void *plan,
                            cudaStream_t s);
 cudaError_t launch_layout(const LayoutArgs &a, cudaStream_t s);
+cudaError_t launch_zero_pad(const Group *groups, int n_groups, int D, uint16_t *buf0, uint16_t *buf1,
+                            cudaStream_t s);
+cudaError_t launch_bwd_swiglu(const Group *groups, int n_groups, int n_rows_total, int H, const uint16_t *GU,
+                              const uint16_t *dA0, float *gate_io, uint16_t *Aw, uint16_t *dGU, cudaStream_t s);
+cudaError_t launch_grad_reduce(float *dst, const float *base, int n_src, int64_t stride_floats, int64_t n_floats,
+                               cudaStream_t s);
 cudaError_t launch_mirror(const void *plan, size_t plan_bytes, const void *summary, size_t sum_bytes,
                           const int32_t *err, void *host_plan, void *host_sum, int32_t *host_err,
                           cudaStream_t s);
@@ -136,6 +142,8 @@ struct DispatchArgs {
   uint16_t *const *peer_x;  // [P] receive rows base of each device (peer-mapped)
   float *const *peer_g;     // [P]
   int32_t *slot_dst;        // [2*B*K] (device, row)
+  const uint16_t *x2;       // optional second row source (backward: the upstream gradient dOut)
+  uint16_t *const *peer_x2; // [P] its receive rows
 };
 cudaError_t launch_dispatch(const DispatchArgs &a, cudaStream_t s);
 
@@ -145,6 +153,8 @@ struct CombineArgs {
   int64_t B;
   int32_t K, D;
   uint16_t *out;
+  const float *const *peer_s;  // optional per-row scalar to pull per slot (backward: dL/dgate)
+  float *slot_out;             // [B*K]
 };
 cudaError_t launch_combine(const CombineArgs &a, cudaStream_t s);
 
@@ -169,5 +179,26 @@ struct GemmArgs {
   int32_t row_align;         // 128: 1-CTA M=128 tiles; 256: 2-CTA (cta_group::2) M=256 tiles
 };
 llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s);
+
+// backward GEMMs (gemm.cu).  kind 0: out[r] = a[r, 0:kdim] · W_e[kdim, nout] (bf16 out, grouped by rows,
+// Group.mblk_start counted in units of mblk_scale 128-row blocks); kind 1: out[e] = a[rows_e]ᵀ · b[rows_e]
+// (fp32 [mdim, nout] per group, K = the group's rows padded to 256, padding rows zero)
+struct BwdArgs {
+  int32_t kind;
+  const uint16_t *a;
+  const uint16_t *b;
+  int64_t rows;
+  int32_t kdim, mdim, nout, n_weights;
+  const uint16_t *b_foreign;  // kind 0: foreign-expert weights (groups with wslot < 0)
+  int32_t n_foreign;
+  void *out_foreign;          // kind 1: output of groups with wslot < 0 (slot -1 - wslot); nullptr:
+                              // every group writes `out` at slot Group.expert
+  const Group *groups;
+  int32_t n_groups;
+  int32_t mblk_scale;
+  void *out;
+  int32_t num_sms;
+};
+llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s);
 
 }  // namespace llep

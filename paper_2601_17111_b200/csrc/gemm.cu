@@ -179,7 +179,7 @@ template <int BN, int MODE>
 __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __grid_constant__ GemmParams p) {
   using C = Cfg<BN>;
   constexpr int S = C::STAGES;
-  constexpr int BNO = MODE == 0 ? BN / 2 : BN;   // output columns per tile
+  constexpr int BNO = MODE != 1 ? BN / 2 : BN;   // output columns per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
           const uint32_t fb = smem_u32(full + stage);
           mbar_expect_tx(fb, C::STAGE);
           tma_load_2d(smem_u32(sA + stage * C::A_BYTES), &p.tmA, fb, kb * BK, ti.row0);
-          if (MODE == 0) {
+          if (MODE != 1) {
             tma_load_2d(smem_u32(sB + stage * C::B_BYTES), wm, fb, kb * BK, wbase);
             tma_load_2d(smem_u32(sB + stage * C::B_BYTES + (BN / 2) * BK * 2), wm, fb, kb * BK,
                         wbase + p.wup_off);
@@ -299,7 +299,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
       const bool row_ok = row < ti.row_end;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
       const int col0 = ti.nb * BNO;
-      if (MODE == 0) {
+      if (MODE == 2) {
+        // raw gate / up pre-activations for the backward recompute: GU[r] = [g (nout) | u (nout)]
+        __nv_bfloat16 *grow = p.out + (size_t)row * 2 * p.nout + col0;
+#pragma unroll 1
+        for (int j = 0; j < BNO; j += 8) {
+          float g[8], u[8];
+          tmem_ld8(taddr + j, g);
+          tmem_ld8(taddr + BNO + j, u);
+          tmem_ld_wait();
+          if (row_ok && col0 + j < p.nout) {
+            uint4 og, ou;
+            __nv_bfloat162 *hg = reinterpret_cast<__nv_bfloat162 *>(&og);
+            __nv_bfloat162 *hu = reinterpret_cast<__nv_bfloat162 *>(&ou);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              hg[i] = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
+              hu[i] = __floats2bfloat162_rn(u[2 * i], u[2 * i + 1]);
+            }
+            *reinterpret_cast<uint4 *>(grow + j) = og;
+            *reinterpret_cast<uint4 *>(grow + p.nout + j) = ou;
+          }
+        }
+      } else if (MODE == 0) {
         __nv_bfloat16 *orow = p.out + (size_t)row * p.nout + col0;
 #pragma unroll 1
         for (int j = 0; j < BNO; j += 8) {
@@ -427,7 +449,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
   constexpr int S = C::STAGES;
   constexpr int TM = 2 * BM;                     // rows per pair tile
   constexpr int BH = BN / 2;                     // B rows staged by each CTA
-  constexpr int BNO = MODE == 0 ? BN / 2 : BN;   // output columns per tile
+  constexpr int BNO = MODE != 1 ? BN / 2 : BN;   // output columns per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -488,7 +510,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
         const TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
         const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
         const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
-        const int brow = MODE == 0 ? wbase + (int)crank * p.wup_off : wbase + (int)crank * BH;
+        const int brow = MODE != 1 ? wbase + (int)crank * p.wup_off : wbase + (int)crank * BH;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const uint32_t fl = smem_u32(full + stage);
@@ -551,7 +573,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       const bool row_ok = row < ti.row_end;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
       const int col0 = ti.nb * BNO;
-      if (MODE == 0) {
+      if (MODE == 2) {
+        // raw gate / up pre-activations for the backward recompute: GU[r] = [g (nout) | u (nout)]
+        __nv_bfloat16 *grow = p.out + (size_t)row * 2 * p.nout + col0;
+#pragma unroll 1
+        for (int j = 0; j < BNO; j += 8) {
+          float g[8], u[8];
+          tmem_ld8(taddr + j, g);
+          tmem_ld8(taddr + BNO + j, u);
+          tmem_ld_wait();
+          if (row_ok && col0 + j < p.nout) {
+            uint4 og, ou;
+            __nv_bfloat162 *hg = reinterpret_cast<__nv_bfloat162 *>(&og);
+            __nv_bfloat162 *hu = reinterpret_cast<__nv_bfloat162 *>(&ou);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              hg[i] = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
+              hu[i] = __floats2bfloat162_rn(u[2 * i], u[2 * i + 1]);
+            }
+            *reinterpret_cast<uint4 *>(grow + j) = og;
+            *reinterpret_cast<uint4 *>(grow + p.nout + j) = ou;
+          }
+        }
+      } else if (MODE == 0) {
         __nv_bfloat16 *orow = p.out + (size_t)row * p.nout + col0;
 #pragma unroll 1
         for (int j = 0; j < BNO; j += 8) {
@@ -641,8 +685,8 @@ llep_status launch(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
     LLEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
-  const int box_w = MODE == 0 ? BN / 2 : BN;
-  const int wrows = MODE == 0 ? 2 * g.nout : g.nout;
+  const int box_w = MODE != 1 ? BN / 2 : BN;
+  const int wrows = MODE != 1 ? 2 * g.nout : g.nout;
   if (!make_map(&prm.tmA, g.a, g.a_rows, g.kdim, BM) ||
       !make_map(&prm.tmW0, g.w_native, (int64_t)g.n_native * wrows, g.kdim, box_w) ||
       !make_map(&prm.tmW1, g.w_foreign ? g.w_foreign : g.w_native,
@@ -651,7 +695,7 @@ llep_status launch(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
     return LLEP_ERR_CUDA;
   }
   prm.wrows = wrows;
-  prm.wup_off = MODE == 0 ? g.nout : 0;
+  prm.wup_off = MODE != 1 ? g.nout : 0;
   prm.n_ntiles = (g.nout + box_w - 1) / box_w;
   grouped_gemm_kernel<BN, MODE><<<g.num_sms, kGemmThreads, C::SMEM, s>>>(prm);
   LLEP_CUDA(cudaGetLastError());
@@ -668,7 +712,7 @@ llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
     attr_set = true;
   }
   const int box_w = BN / 2;
-  const int wrows = MODE == 0 ? 2 * g.nout : g.nout;
+  const int wrows = MODE != 1 ? 2 * g.nout : g.nout;
   if (!make_map(&prm.tmA, g.a, g.a_rows, g.kdim, BM) ||
       !make_map(&prm.tmW0, g.w_native, (int64_t)g.n_native * wrows, g.kdim, box_w) ||
       !make_map(&prm.tmW1, g.w_foreign ? g.w_foreign : g.w_native,
@@ -677,8 +721,8 @@ llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
     return LLEP_ERR_CUDA;
   }
   prm.wrows = wrows;
-  prm.wup_off = MODE == 0 ? g.nout : 0;
-  prm.n_ntiles = (g.nout + (MODE == 0 ? BN / 2 : BN) - 1) / (MODE == 0 ? BN / 2 : BN);
+  prm.wup_off = MODE != 1 ? g.nout : 0;
+  prm.n_ntiles = (g.nout + (MODE != 1 ? BN / 2 : BN) - 1) / (MODE != 1 ? BN / 2 : BN);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(g.num_sms & ~1));
   cfg.blockDim = dim3(kGemmThreads);
@@ -695,7 +739,315 @@ llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
   return LLEP_OK;
 }
 
+
+// ------------------------------------------------------------------------ backward GEMMs (f1)
+// The backward pass contracts the expert weights along the other dimension and the
+// activations along the token dimension, so its operands are MN-major in shared memory: TMA boxes
+// of 64 MN-elements (128 B, swizzled) x 64 K-rows, one 8 KB block per 64-wide MN chunk.  UMMA
+// descriptor for such a tile: LBO = distance between MN chunks (8 KB), SBO = distance between
+// 8-row K groups (1 KB); a 16-deep K step advances the start address by 16 rows (2 KB).
+//   KIND 0 (rows):  C[r, n] = Σ_k A[r, k] · W_e[k, n]      A K-major rows, W row-major [K][N]
+//                   (dA = dY·W_down with W_down [D][H]; dX = dGU·W13 with W13 [2H][D]); bf16 out
+//   KIND 1 (wgrad): C_e[m, n] = Σ_{r in group e} A[r, m] · B[r, n]   both MN-major, K = tokens
+//                   (dW_down = dYᵀ·a, dW13 = dGUᵀ·X); fp32 out per group
+constexpr int kBwdBN = 256;
+constexpr int kBwdA = BM * BK * 2;        // 16 KB (K-major 128 rows, or 2 MN chunks)
+constexpr int kBwdB = kBwdBN * BK * 2;    // 32 KB (4 MN chunks)
+constexpr int kBwdStage = kBwdA + kBwdB;
+constexpr int kBwdStages = 4;
+constexpr int kBwdSmem = kBwdStages * kBwdStage + 1024 + 256;
+
+struct BwdParams {
+  CUtensorMap tmA, tmB, tmB1;   // tmB1: foreign-expert weights (KIND 0, groups with wslot < 0)
+  const Group *groups;
+  int32_t n_groups;
+  int32_t kdim;          // KIND 0: contraction length (rows of W_e)
+  int32_t mdim;          // KIND 1: output rows per group
+  int32_t nout;          // output columns
+  int32_t n_mt, n_nt;    // tiles per group (KIND 1: m x n) ; KIND 0: n tiles
+  int32_t mblk_scale;    // KIND 0: 128-row blocks per Group.mblk_start unit
+  void *out;
+  void *out_foreign;     // KIND 1: output of foreign groups (wslot < 0), nullptr -> out[expert]
+};
+
+__device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((8192 >> 4) & 0x3FFF) << 16;     // LBO: next 64-wide MN chunk
+  d |= (uint64_t)(1024 >> 4) << 32;                 // SBO: next 8-row K group
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+struct BwdTile {
+  int row0, row_end, m0, n0, g, nk;
+};
+
+template <int KIND>
+__device__ __forceinline__ BwdTile decode_bwd(int t, const BwdParams &p, const int *s_mblk) {
+  BwdTile ti;
+  if (KIND == 0) {
+    const int mb = t / p.n_nt;
+    ti.n0 = (t - mb * p.n_nt) * kBwdBN;
+    int lo = 0, hi = p.n_groups - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_mblk[mid] * p.mblk_scale <= mb) lo = mid;
+      else hi = mid - 1;
+    }
+    const Group g = p.groups[lo];
+    ti.g = lo;
+    ti.row0 = g.row_base + (mb - s_mblk[lo] * p.mblk_scale) * BM;
+    ti.row_end = g.row_base + g.n_rows;
+    ti.m0 = 0;
+    ti.nk = (p.kdim + BK - 1) / BK;
+  } else {
+    const int per = p.n_mt * p.n_nt;
+    ti.g = t / per;
+    const int r = t - ti.g * per;
+    const int mt = r / p.n_nt;
+    ti.m0 = mt * BM;
+    ti.n0 = (r - mt * p.n_nt) * kBwdBN;
+    const Group g = p.groups[ti.g];
+    ti.row0 = g.row_base;
+    ti.row_end = g.row_base + g.n_rows;
+    ti.nk = (g.n_rows + 255) / 256 * (256 / BK);   // padded rows are zero in both operands
+  }
+  return ti;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_kernel(const __grid_constant__ BwdParams p) {
+  constexpr int S = kBwdStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + S * kBwdA;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S * kBwdStage);
+  uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+  __shared__ int s_mblk[kMaxGroups];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int g = threadIdx.x; g < p.n_groups; g += kGemmThreads) s_mblk[g] = p.groups[g].mblk_start;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(smem_u32(full + i), 1);
+      mbar_init(smem_u32(empty + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(tfull + i), 1);
+      mbar_init(smem_u32(tempty + i), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(2 * kAccCols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  int total_tiles = 0;
+  if (p.n_groups > 0) {
+    if (KIND == 0) {
+      const Group last = p.groups[p.n_groups - 1];
+      total_tiles = (last.mblk_start * p.mblk_scale + (last.n_rows + BM - 1) / BM) * p.n_nt;
+    } else {
+      total_tiles = p.n_groups * p.n_mt * p.n_nt;
+    }
+  }
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const BwdTile ti = decode_bwd<KIND>(t, p, s_mblk);
+        const int ws = KIND == 0 ? p.groups[ti.g].wslot : 0;
+        const int wrow = (ws >= 0 ? ws : -1 - ws) * p.kdim;
+        const CUtensorMap *bm = ws >= 0 ? &p.tmB : &p.tmB1;
+        for (int kb = 0; kb < ti.nk; ++kb) {
+          mbar_wait(smem_u32(empty + stage), phase ^ 1);
+          const uint32_t fb = smem_u32(full + stage);
+          mbar_expect_tx(fb, kBwdStage);
+          const uint32_t a_dst = smem_u32(sA + stage * kBwdA);
+          const uint32_t b_dst = smem_u32(sB + stage * kBwdB);
+          if (KIND == 0) {
+            tma_load_2d(a_dst, &p.tmA, fb, kb * BK, ti.row0);                 // K-major rows
+#pragma unroll
+            for (int c = 0; c < kBwdBN / 64; ++c)                            // W_e[k, n] chunks
+              tma_load_2d(b_dst + c * 8192, bm, fb, ti.n0 + c * 64, wrow + kb * BK);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c)
+              tma_load_2d(a_dst + c * 8192, &p.tmA, fb, ti.m0 + c * 64, ti.row0 + kb * BK);
+#pragma unroll
+            for (int c = 0; c < kBwdBN / 64; ++c)
+              tma_load_2d(b_dst + c * 8192, &p.tmB, fb, ti.n0 + c * 64, ti.row0 + kb * BK);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((KIND == 1 ? 1u : 0u) << 15) |
+                             (1u << 16) | ((uint32_t)(kBwdBN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+        const BwdTile ti = decode_bwd<KIND>(t, p, s_mblk);
+        const int acc = it & 1;
+        mbar_wait(smem_u32(tempty + acc), ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        for (int kb = 0; kb < ti.nk; ++kb) {
+          mbar_wait(smem_u32(full + stage), phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * kBwdA);
+          const uint32_t b0 = smem_u32(sB + stage * kBwdB);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = KIND == 0 ? smem_desc(a0 + kk * 32) : smem_desc_mn(a0 + kk * 2048);
+            tc_mma(d_tmem, ad, smem_desc_mn(b0 + kk * 2048), idesc, (kb | kk) != 0);
+          }
+          tc_commit(smem_u32(empty + stage));
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(smem_u32(tfull + acc));
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    int it = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const BwdTile ti = decode_bwd<KIND>(t, p, s_mblk);
+      mbar_wait(smem_u32(tfull + acc), (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
+      if (KIND == 0) {
+        const int row = ti.row0 + q * 32 + lane;
+        const bool ok = row < ti.row_end;
+        __nv_bfloat16 *orow = reinterpret_cast<__nv_bfloat16 *>(p.out) + (size_t)row * p.nout + ti.n0;
+#pragma unroll 1
+        for (int j = 0; j < kBwdBN; j += 8) {
+          float v[8];
+          tmem_ld8(taddr + j, v);
+          tmem_ld_wait();
+          if (ok && ti.n0 + j < p.nout) {
+            uint4 o;
+            __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            *reinterpret_cast<uint4 *>(orow + j) = o;
+          }
+        }
+      } else {
+        const int m = ti.m0 + q * 32 + lane;
+        const bool ok = m < p.mdim;
+        const Group gg = p.groups[ti.g];
+        float *obase = reinterpret_cast<float *>(p.out);
+        size_t slot = (size_t)gg.expert;
+        if (p.out_foreign) {
+          slot = gg.wslot >= 0 ? (size_t)gg.wslot : (size_t)(-1 - gg.wslot);
+          if (gg.wslot < 0) obase = reinterpret_cast<float *>(p.out_foreign);
+        }
+        float *orow = obase + (slot * p.mdim + m) * p.nout + ti.n0;
+#pragma unroll 1
+        for (int j = 0; j < kBwdBN; j += 8) {
+          float v[8];
+          tmem_ld8(taddr + j, v);
+          tmem_ld_wait();
+          if (ok && ti.n0 + j < p.nout) {
+            *reinterpret_cast<float4 *>(orow + j) = make_float4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<float4 *>(orow + j + 4) = make_float4(v[4], v[5], v[6], v[7]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(2 * kAccCols) : "memory");
+}
+
+bool make_map_box(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, int box_cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  if (rows < 1) rows = 1;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
+
+llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s) {
+  if (a.nout % 8 || a.kdim % 8 || a.mdim % 8) {
+    set_error("backward GEMM needs dims %% 8 == 0");
+    return LLEP_ERR_INVALID;
+  }
+  BwdParams p;
+  memset(&p, 0, sizeof(p));
+  p.groups = a.groups;
+  p.n_groups = a.n_groups;
+  p.kdim = a.kdim;
+  p.mdim = a.mdim;
+  p.nout = a.nout;
+  p.n_nt = (a.nout + kBwdBN - 1) / kBwdBN;
+  p.n_mt = (a.mdim + BM - 1) / BM;
+  p.mblk_scale = a.mblk_scale;
+  p.out = a.out;
+  p.out_foreign = a.out_foreign;
+  bool ok;
+  if (a.kind == 0) {
+    ok = make_map_box(&p.tmA, a.a, a.rows, a.kdim, BK, BM) &&
+         make_map_box(&p.tmB, a.b, (int64_t)a.n_weights * a.kdim, a.nout, 64, BK) &&
+         make_map_box(&p.tmB1, a.b_foreign ? a.b_foreign : a.b,
+                      (int64_t)(a.b_foreign ? a.n_foreign : a.n_weights) * a.kdim, a.nout, 64, BK);
+  } else {
+    ok = make_map_box(&p.tmA, a.a, a.rows, a.mdim, 64, BK) &&
+         make_map_box(&p.tmB, a.b, a.rows, a.nout, 64, BK) &&
+         make_map_box(&p.tmB1, a.b, a.rows, a.nout, 64, BK);
+  }
+  if (!ok) {
+    set_error("cuTensorMapEncodeTiled failed for a backward GEMM operand");
+    return LLEP_ERR_CUDA;
+  }
+  static bool attr[2] = {false, false};
+  if (!attr[a.kind]) {
+    LLEP_CUDA(cudaFuncSetAttribute(a.kind == 0 ? gemm_bwd_kernel<0> : gemm_bwd_kernel<1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem));
+    attr[a.kind] = true;
+  }
+  if (a.kind == 0) gemm_bwd_kernel<0><<<a.num_sms, kGemmThreads, kBwdSmem, s>>>(p);
+  else gemm_bwd_kernel<1><<<a.num_sms, kGemmThreads, kBwdSmem, s>>>(p);
+  LLEP_CUDA(cudaGetLastError());
+  return LLEP_OK;
+}
+
+namespace {}  // (run_grouped_gemm below)
 
 llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   if (g.kdim % 8 != 0 || g.nout % 8 != 0) {
@@ -719,6 +1071,12 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
       if (g.nout % 96 == 0) return launch_pair<192, 0>(g, prm, s);
       return launch_pair<256, 0>(g, prm, s);
     }
+    if (g.mode == 2) {
+      if (g.nout % 128 == 0) return launch_pair<256, 2>(g, prm, s);
+      if (g.nout % 120 == 0) return launch_pair<240, 2>(g, prm, s);
+      if (g.nout % 96 == 0) return launch_pair<192, 2>(g, prm, s);
+      return launch_pair<256, 2>(g, prm, s);
+    }
     if (g.nout % 256 == 0) return launch_pair<256, 1>(g, prm, s);
     if (g.nout % 240 == 0) return launch_pair<240, 1>(g, prm, s);
     if (g.nout % 192 == 0) return launch_pair<192, 1>(g, prm, s);
@@ -730,6 +1088,12 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
     if (g.nout % 120 == 0) return launch<240, 0>(g, prm, s);
     if (g.nout % 96 == 0) return launch<192, 0>(g, prm, s);
     return launch<256, 0>(g, prm, s);
+  }
+  if (g.mode == 2) {
+    if (g.nout % 128 == 0) return launch<256, 2>(g, prm, s);
+    if (g.nout % 120 == 0) return launch<240, 2>(g, prm, s);
+    if (g.nout % 96 == 0) return launch<192, 2>(g, prm, s);
+    return launch<256, 2>(g, prm, s);
   }
   if (g.nout % 256 == 0) return launch<256, 1>(g, prm, s);
   if (g.nout % 240 == 0) return launch<240, 1>(g, prm, s);

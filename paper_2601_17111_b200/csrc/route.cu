@@ -178,23 +178,26 @@ __global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_kernel(DispatchA
     if (dev >= 0) a.peer_g[dev][row] = a.w[j];
   }
   const int nv = a.D / 8;  // 16-byte vectors per row
-  const int4 *src = reinterpret_cast<const int4 *>(a.x) + t * nv;
-  for (int i0 = 0; i0 < nv; i0 += 32 * 4) {
-    int4 v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * 32 + lane;
-      if (i < nv) v[u] = __ldg(src + i);
-    }
-    for (int k = 0; k < K; ++k) {
-      const int d = __shfl_sync(0xffffffffu, dev, k);
-      const int r = __shfl_sync(0xffffffffu, row, k);
-      if (d < 0) continue;
-      int4 *dst = reinterpret_cast<int4 *>(a.peer_x[d]) + (int64_t)r * nv;
+  for (int src_i = 0; src_i < (a.x2 ? 2 : 1); ++src_i) {
+    const int4 *src = reinterpret_cast<const int4 *>(src_i ? a.x2 : a.x) + t * nv;
+    uint16_t *const *peer = src_i ? a.peer_x2 : a.peer_x;
+    for (int i0 = 0; i0 < nv; i0 += 32 * 4) {
+      int4 v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = i0 + u * 32 + lane;
-        if (i < nv) dst[i] = v[u];
+        if (i < nv) v[u] = __ldg(src + i);
+      }
+      for (int k = 0; k < K; ++k) {
+        const int d = __shfl_sync(0xffffffffu, dev, k);
+        const int r = __shfl_sync(0xffffffffu, row, k);
+        if (d < 0) continue;
+        int4 *dst = reinterpret_cast<int4 *>(peer[d]) + (int64_t)r * nv;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * 32 + lane;
+          if (i < nv) dst[i] = v[u];
+        }
       }
     }
   }
@@ -235,6 +238,7 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
     dev = a.slot_dst[2 * (t * K + lane)];
     row = a.slot_dst[2 * (t * K + lane) + 1];
   }
+  if (a.peer_s && lane < K) a.slot_out[t * K + lane] = dev >= 0 ? a.peer_s[dev][row] : 0.f;
   const int nv = a.D / 8;
   const int4 *src[KM];
 #pragma unroll
@@ -271,6 +275,109 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
   }
 }
 
+// -------------------------------------------------------------------------- backward (f1)
+// Zero the padding rows of this device's groups (rows past n_rows up to the next multiple of 256)
+// in up to two row buffers: the weight-gradient GEMMs contract over whole 256-row blocks.
+__global__ void zero_pad_kernel(const Group *__restrict__ groups, int D, uint16_t *buf0, uint16_t *buf1) {
+  const Group g = groups[blockIdx.x];
+  const int pad_end = g.row_base + (g.n_rows + 255) / 256 * 256;
+  const int nv = D / 8;
+  for (int r = g.row_base + g.n_rows; r < pad_end; ++r) {
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+      reinterpret_cast<int4 *>(buf0)[(int64_t)r * nv + i] = make_int4(0, 0, 0, 0);
+      if (buf1) reinterpret_cast<int4 *>(buf1)[(int64_t)r * nv + i] = make_int4(0, 0, 0, 0);
+    }
+  }
+}
+
+// SwiGLU backward for one received row r (one warp per row), from the recomputed pre-activations
+// GU[r] = [g | u], da0 = dY_unscaled · W_down and the row's gate w:
+//   a = silu(g) u,  da = w da0,  dg = da u silu'(g),  du = da silu(g),  dw = <a, da0>
+// writes A'[r] = w a (for dW_down = dO_rowsᵀ · A'), dGU[r] = [dg | du], and dw into gate[r].
+// Padding rows of each group (up to 256) get zeros.
+__global__ void bwd_swiglu_kernel(const Group *__restrict__ groups, int n_groups, int n_rows_total,
+                                  int H, const uint16_t *__restrict__ GU, const uint16_t *__restrict__ dA0,
+                                  float *__restrict__ gate_io, uint16_t *__restrict__ Aw,
+                                  uint16_t *__restrict__ dGU) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= n_rows_total) return;
+  int lo = 0, hi = n_groups - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (groups[mid].row_base <= r) lo = mid;
+    else hi = mid - 1;
+  }
+  const Group g = groups[lo];
+  const bool real = r >= g.row_base && r < g.row_base + g.n_rows;
+  const bool pad = r >= g.row_base + g.n_rows && r < g.row_base + (g.n_rows + 255) / 256 * 256;
+  if (!real && !pad) return;
+  const int nv = H / 8;
+  const int4 *gu = reinterpret_cast<const int4 *>(GU) + (int64_t)r * 2 * nv;
+  const int4 *d0 = reinterpret_cast<const int4 *>(dA0) + (int64_t)r * nv;
+  int4 *aw = reinterpret_cast<int4 *>(Aw) + (int64_t)r * nv;
+  int4 *dgu = reinterpret_cast<int4 *>(dGU) + (int64_t)r * 2 * nv;
+  if (!real) {
+    for (int i = lane; i < nv; i += 32) {
+      aw[i] = make_int4(0, 0, 0, 0);
+      dgu[i] = make_int4(0, 0, 0, 0);
+      dgu[nv + i] = make_int4(0, 0, 0, 0);
+    }
+    return;
+  }
+  const float w = gate_io[r];
+  float dot = 0.f;
+  for (int i = lane; i < nv; i += 32) {
+    const int4 gv = gu[i], uv = gu[nv + i], dv = d0[i];
+    const __nv_bfloat162 *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gv);
+    const __nv_bfloat162 *u2 = reinterpret_cast<const __nv_bfloat162 *>(&uv);
+    const __nv_bfloat162 *d2 = reinterpret_cast<const __nv_bfloat162 *>(&dv);
+    int4 ao, go, uo;
+    __nv_bfloat162 *a2 = reinterpret_cast<__nv_bfloat162 *>(&ao);
+    __nv_bfloat162 *gg = reinterpret_cast<__nv_bfloat162 *>(&go);
+    __nv_bfloat162 *uu = reinterpret_cast<__nv_bfloat162 *>(&uo);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 gf = __bfloat1622float2(g2[q]), uf = __bfloat1622float2(u2[q]), df = __bfloat1622float2(d2[q]);
+      float ar[2], dgr[2], dur[2];
+      const float gz[2] = {gf.x, gf.y}, uz[2] = {uf.x, uf.y}, dz[2] = {df.x, df.y};
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const float sg = 1.f / (1.f + __expf(-gz[c]));
+        const float si = gz[c] * sg;
+        const float a = si * uz[c];
+        const float da = w * dz[c];
+        ar[c] = a;
+        dot += a * dz[c];
+        dgr[c] = da * uz[c] * sg * (1.f + gz[c] * (1.f - sg));
+        dur[c] = da * si;
+      }
+      a2[q] = __floats2bfloat162_rn(w * ar[0], w * ar[1]);
+      gg[q] = __floats2bfloat162_rn(dgr[0], dgr[1]);
+      uu[q] = __floats2bfloat162_rn(dur[0], dur[1]);
+    }
+    aw[i] = ao;
+    dgu[i] = go;
+    dgu[nv + i] = uo;
+  }
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  if (lane == 0) gate_io[r] = dot;   // dL/dw of this (token, slot) row
+}
+
+// dst[i] += Σ_s src_s[i] in the listed order (the native device adds the weight-gradient partials
+// its replicas returned, in ascending source-device order).
+__global__ void grad_reduce_kernel(float *__restrict__ dst, const float *__restrict__ base, int n_src,
+                                   int64_t stride4, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 acc = reinterpret_cast<float4 *>(dst)[i];
+    for (int s = 0; s < n_src; ++s) {
+      const float4 v = reinterpret_cast<const float4 *>(base)[s * stride4 + i];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    reinterpret_cast<float4 *>(dst)[i] = acc;
+  }
+}
+
 // ----------------------------------------------------------------------- host read-back
 // Copies the plan blob, the layout summary and the error flags into mapped pinned host memory
 // with plain stores (zero-copy), so the one host synchronisation of the layer never queues
@@ -285,6 +392,29 @@ __global__ void mirror_kernel(const uint32_t *__restrict__ plan, int n_plan_word
 }
 
 }  // namespace
+
+cudaError_t launch_zero_pad(const Group *groups, int n_groups, int D, uint16_t *buf0, uint16_t *buf1,
+                            cudaStream_t s) {
+  if (n_groups <= 0) return cudaSuccess;
+  zero_pad_kernel<<<n_groups, 256, 0, s>>>(groups, D, buf0, buf1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_swiglu(const Group *groups, int n_groups, int n_rows_total, int H, const uint16_t *GU,
+                              const uint16_t *dA0, float *gate_io, uint16_t *Aw, uint16_t *dGU, cudaStream_t s) {
+  if (n_rows_total <= 0 || n_groups <= 0) return cudaSuccess;
+  const int warps = 8;
+  bwd_swiglu_kernel<<<(n_rows_total + warps - 1) / warps, warps * 32, 0, s>>>(groups, n_groups, n_rows_total, H,
+                                                                            GU, dA0, gate_io, Aw, dGU);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grad_reduce(float *dst, const float *base, int n_src, int64_t stride_floats, int64_t n_floats,
+                               cudaStream_t s) {
+  if (n_src <= 0) return cudaSuccess;
+  grad_reduce_kernel<<<296, 256, 0, s>>>(dst, base, n_src, stride_floats / 4, n_floats / 4);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_mirror(const void *plan, size_t plan_bytes, const void *summary, size_t sum_bytes,
                           const int32_t *err, void *host_plan, void *host_sum, int32_t *host_err,

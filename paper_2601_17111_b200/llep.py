@@ -51,7 +51,8 @@ class Stats(ctypes.Structure):
 class Requirements(ctypes.Structure):
     _fields_ = [("rows_needed", ctypes.c_int64), ("foreign_needed", ctypes.c_int32), ("fits", ctypes.c_int32),
                 ("my_rows", ctypes.c_int64), ("my_groups", ctypes.c_int32), ("fallback_ep", ctypes.c_int32),
-                ("force_count", ctypes.c_int32), ("n_transfers", ctypes.c_int32)]
+                ("force_count", ctypes.c_int32), ("n_transfers", ctypes.c_int32),
+                ("grad_slots_needed", ctypes.c_int32)]
 
 
 _vp, _i32, _i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
@@ -66,7 +67,9 @@ _SIGS = {
     "llep_context_destroy": (None, [_vp]),
     "llep_context_ipc_handle": (ctypes.c_int, [_vp, _vp]),
     "llep_context_open_peers": (ctypes.c_int, [_vp, _vp, _i32]),
-    "llep_context_reserve": (ctypes.c_int, [_vp, _i64, _i32]),
+    "llep_context_reserve": (ctypes.c_int, [_vp, _i64, _i32, _i32]),
+    "llep_context_enable_backward": (ctypes.c_int, [_vp]),
+    "llep_moe_backward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "llep_context_device_bytes": (_i64, [_vp]),
     "llep_context_set_memory_cap": (ctypes.c_int, [_vp, _i64]),
     "llep_prepare": (ctypes.c_int, [_vp, _vp, _i64, ctypes.POINTER(Params), _i32, _vp,
@@ -75,6 +78,7 @@ _SIGS = {
     "llep_debug_copy": (ctypes.c_int, [_vp, _i32, _vp, _i64, _vp]),
     "llep_context_set_timing": (ctypes.c_int, [_vp, _i32]),
     "llep_context_stats": (ctypes.c_int, [_vp, ctypes.c_void_p, _i32]),
+    "llep_gemm_bwd": (ctypes.c_int, [_i32, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
     "llep_grouped_gemm": (ctypes.c_int, [_i32, _vp, _i64, _i32, _vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
 }
 EXPORTS = tuple(_SIGS)
@@ -213,8 +217,14 @@ class Context:
         blob = b"".join(allh)
         _check(_lib.llep_context_open_peers(self._h, blob, self.P))
 
-    def reserve(self, rows: int, foreign: int) -> None:
-        _check(_lib.llep_context_reserve(self._h, int(rows), int(foreign)))
+    def reserve(self, rows: int, foreign: int, grad_slots: int = 0) -> None:
+        _check(_lib.llep_context_reserve(self._h, int(rows), int(foreign), int(grad_slots)))
+        if self.P > 1:
+            self.exchange_handles()
+
+    def enable_backward(self) -> None:
+        """Row f1: arena regions for dout rows and returned weight-gradient partials (collective)."""
+        _check(_lib.llep_context_enable_backward(self._h))
         if self.P > 1:
             self.exchange_handles()
 
@@ -245,7 +255,7 @@ class Context:
                                  ctypes.byref(req), _stream_ptr()))
         if not req.fits:
             # identical on every rank (replicated plan): grow symmetrically, re-map peers
-            self.reserve(int(req.rows_needed * 1.0), int(req.foreign_needed))
+            self.reserve(int(req.rows_needed), int(req.foreign_needed), int(req.grad_slots_needed))
             req.fits = 1
         self.last_req = req
         return plan_out, req
@@ -263,6 +273,23 @@ class Context:
                                      w13.data_ptr(), w2.data_ptr(), plan.data_ptr(), out.data_ptr(),
                                      _stream_ptr()))
         return out
+
+    def backward(self, x, topk_ids, topk_w, dout, w13, w2, plan, dx=None, dgates=None, dw13=None, dw2=None):
+        """llep_moe_backward under `plan` (from prepare on these topk_ids): returns
+        (dx [B, D] bf16, dgates [B, K] fp32, dw13 [M, 2H, D] fp32, dw2 [M, D, H] fp32)."""
+        import torch
+        B = x.shape[0]
+        dev = x.device
+        assert dout.dtype == torch.bfloat16 and dout.is_contiguous() and dout.shape == x.shape
+        dx = torch.empty_like(x) if dx is None else dx
+        dgates = torch.empty((B, self.K), dtype=torch.float32, device=dev) if dgates is None else dgates
+        dw13 = torch.empty((self.M, 2 * self.H, self.D), dtype=torch.float32, device=dev) if dw13 is None else dw13
+        dw2 = torch.empty((self.M, self.D, self.H), dtype=torch.float32, device=dev) if dw2 is None else dw2
+        _check(_lib.llep_moe_backward(self._h, x.data_ptr(), topk_ids.data_ptr(), topk_w.data_ptr(),
+                                      dout.data_ptr(), B, w13.data_ptr(), w2.data_ptr(), plan.data_ptr(),
+                                      dx.data_ptr(), dgates.data_ptr(), dw13.data_ptr(), dw2.data_ptr(),
+                                      _stream_ptr()))
+        return dx, dgates, dw13, dw2
 
     def __call__(self, x, topk_ids, topk_w, w13, w2, alpha=1.0, min_chunk=1024, lam=1.3, ep=False,
                  plan_out=None, out=None):
@@ -291,4 +318,20 @@ def grouped_gemm(mode: int, a, w, groups: Sequence[Tuple[int, int, int]], nout: 
     _check(_lib.llep_grouped_gemm(mode | (2 if pair else 0), a.data_ptr(), rows, kdim, w.data_ptr(), w.shape[0], nout,
                                   g.ctypes.data, len(groups), gate.data_ptr() if gate is not None else None,
                                   out.data_ptr(), _stream_ptr()))
+    return out
+
+
+def gemm_bwd(kind: int, a, b, groups: Sequence[Tuple[int, int, int]], nout: int, kdim_or_mdim: int,
+             n_weights: int, out=None):
+    """llep_gemm_bwd (see llep.h): kind 0 -> bf16 [rows, nout]; kind 1 -> fp32 [n_weights, mdim, nout]."""
+    import torch
+    rows = a.shape[0]
+    if out is None:
+        if kind == 0:
+            out = torch.zeros((rows, nout), dtype=torch.bfloat16, device=a.device)
+        else:
+            out = torch.zeros((n_weights, kdim_or_mdim, nout), dtype=torch.float32, device=a.device)
+    g = np.ascontiguousarray(np.asarray([[e, rb, n, 0] for (e, rb, n) in groups], dtype=np.int32).reshape(-1))
+    _check(_lib.llep_gemm_bwd(kind, a.data_ptr(), b.data_ptr(), rows, kdim_or_mdim, nout, n_weights,
+                              g.ctypes.data, len(groups), out.data_ptr(), _stream_ptr()))
     return out

@@ -40,9 +40,18 @@ def worker(rank, P, cfg, pct, nhot, outdir, sample):
     torch.cuda.synchronize()
     assert torch.equal(out_llep, out_llep2), "iteration-to-iteration mismatch"
     n = sample if sample > 0 else out_llep.shape[0]
+    extra = {}
+    if os.environ.get("LLEP_TEST_BWD") == "1":
+        ctx.enable_backward()
+        dout = W.tokens_torch(sh.tokens_per_rank, sh.d_model, rank + 1000, f"cuda:{dev}", 21)
+        plan_b, _ = ctx.prepare(ids, alpha, m, lam)
+        dx, dg, dw13, dw2 = ctx.backward(x, ids, gates, dout, w13, w2, plan_b)
+        torch.cuda.synchronize()
+        extra = dict(dx=dx[:n].float().cpu().numpy(), dgates=dg[:n].cpu().numpy(), dw13=dw13.cpu().numpy(),
+                     dw2=dw2.cpu().numpy())
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), llep=out_llep[:n].float().cpu().numpy(),
              ep=out_ep[:n].float().cpu().numpy(), plan=plan_np,
-             same=np.array(bool(torch.equal(out_llep, out_ep))))
+             same=np.array(bool(torch.equal(out_llep, out_ep))), **extra)
     dist.barrier()
     ctx.close()
     dist.destroy_process_group()

@@ -1,0 +1,149 @@
+"""Row f1 (backward pass) on the GPU through llep_moe_backward vs the float64 oracle O5."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+import layer_case as LC  # noqa: E402
+from synth import workload as W  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2601_17111_b200 import llep
+    return llep
+
+
+def _rel(y, r):
+    y = np.asarray(y, dtype=np.float64)
+    r = np.asarray(r, dtype=np.float64)
+    mr = np.abs(y - r).max() / max(np.abs(r).max(), 1e-30)
+    l2 = np.linalg.norm(y - r) / max(np.linalg.norm(r), 1e-30)
+    return mr, l2
+
+
+def _dout(sh, rank, seed):
+    return W.tokens_bits(sh.tokens_per_rank, sh.d_model, rank + 1000, seed)
+
+
+def _check_grads(sh, got, ref_dx, ref_dg, ref_dW, experts, native_base):
+    dx, dg, dw13, dw2 = got
+    mr, l2 = _rel(dx, ref_dx)
+    assert mr <= 2e-2 and l2 <= 5e-3, ("dx", mr, l2)
+    mr, l2 = _rel(dg, ref_dg)
+    assert l2 <= 5e-3, ("dgates", mr, l2)
+    H = sh.d_ff
+    for e in experts:
+        el = e - native_base
+        if e in ref_dW:
+            wg, wu, wd = ref_dW[e]
+            for name, y, r in (("dW_gate", dw13[el, :H], wg), ("dW_up", dw13[el, H:], wu), ("dW_down", dw2[el], wd)):
+                mr, l2 = _rel(y, r)
+                assert l2 <= 5e-3 and mr <= 2e-2, (name, e, mr, l2)
+        else:
+            assert not dw13[el].any() and not dw2[el].any(), e
+
+
+@pytest.mark.parametrize("pct,nhot", [(95, 1), (None, 0)])
+def test_backward_p1_tiny(L, pct, nhot):
+    from oracle import backward as O5
+    base = W.CONFIGS["tiny"]
+    sh = W.LayerShape(base.n_experts, base.top_k, base.d_model, base.d_ff, base.tokens_per_rank, 1)
+    seed = 13
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, pct, nhot, seed, "cuda")
+    dout_bits = _dout(sh, 0, seed)
+    dout = torch.from_numpy(dout_bits.view(np.int16)).cuda().view(torch.bfloat16)
+    ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, 1, 0, 0, sh.tokens_per_rank)
+    ctx.enable_backward()
+    plan, _ = ctx.prepare(ids)
+    got = [t.float().cpu().numpy() for t in ctx.backward(x, ids, gates, dout, w13, w2, plan)]
+    ws = LC.OracleWeights(sh.d_model, sh.d_ff, seed)
+    xr = W.bf16_bits_to_f64(W.tokens_bits(sh.tokens_per_rank, sh.d_model, 0, seed))
+    dx, dg, dW = O5.moe_backward(xr, ids_np, g_np.astype(np.float64), W.bf16_bits_to_f64(dout_bits), ws)
+    _check_grads(sh, got, dx, dg, dW, range(sh.n_experts), 0)
+    ctx.close()
+
+
+def test_backward_g120_p1_sampled(L):
+    """G120 shape at P=1: dx / dgates on sampled tokens, full weight gradients of three cold experts
+    (every row routed to them), against O5."""
+    from oracle import backward as O5
+    base = W.CONFIGS["g120"]
+    sh = W.LayerShape(base.n_experts, base.top_k, base.d_model, base.d_ff, base.tokens_per_rank, 1)
+    seed = 17
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, 95, 1, seed, "cuda")
+    dout_bits = _dout(sh, 0, seed)
+    dout = torch.from_numpy(dout_bits.view(np.int16)).cuda().view(torch.bfloat16)
+    ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, 1, 0, 0, sh.tokens_per_rank)
+    ctx.enable_backward()
+    plan, _ = ctx.prepare(ids)
+    dx, dg, dw13, dw2 = ctx.backward(x, ids, gates, dout, w13, w2, plan)
+    torch.cuda.synchronize()
+    ws = LC.OracleWeights(sh.d_model, sh.d_ff, seed)
+    # tokens with all slots in experts 0..7 (dx, dgates) -- a sample
+    ok = np.nonzero((ids_np < 8).all(1))[0][:24]
+    xr = W.bf16_bits_to_f64(W.token_rows_bits(ok, sh.d_model, 0, seed))
+    do = W.bf16_bits_to_f64(dout_bits[ok])
+    rdx, rdg, _ = O5.moe_backward(xr, ids_np[ok], g_np[ok].astype(np.float64), do, ws)
+    mr, l2 = _rel(dx[torch.from_numpy(ok).cuda()].float().cpu().numpy(), rdx)
+    assert mr <= 2e-2 and l2 <= 5e-3, ("dx", mr, l2)
+    mr, l2 = _rel(dg[torch.from_numpy(ok).cuda()].cpu().numpy(), rdg)
+    assert l2 <= 5e-3, ("dgates", mr, l2)
+    # weight gradients of experts 5, 6, 7: all their rows
+    for e in (5, 6, 7):
+        tt = np.nonzero((ids_np == e).any(1))[0]
+        idm = np.where(ids_np[tt] == e, e, -1)
+        gm = np.where(ids_np[tt] == e, g_np[tt], 0.0)
+        xr = W.bf16_bits_to_f64(W.token_rows_bits(tt, sh.d_model, 0, seed))
+        do = W.bf16_bits_to_f64(dout_bits[tt])
+        # slots of other experts contribute nothing to dW[e]: route them to e with gate 0 is NOT
+        # neutral for dx, so compute the expert directly
+        slots = np.argwhere(idm == e)
+        X = xr[slots[:, 0]]
+        dY = gm[slots[:, 0], slots[:, 1], None] * do[slots[:, 0]]
+        _, _, (wg, wu, wd) = O5.expert_backward(X, dY, ws(e))
+        for name, y, r in (("dW_gate", dw13[e, :sh.d_ff], wg), ("dW_up", dw13[e, sh.d_ff:], wu), ("dW_down", dw2[e], wd)):
+            mr, l2 = _rel(y.cpu().numpy(), r)
+            assert l2 <= 5e-3 and mr <= 2e-2, (name, e, mr, l2)
+    ctx.close()
+
+
+@pytest.mark.parametrize("P,pct,nhot,params", [
+    (2, 95, 1, (1.0, 16, 1.0)),
+    (4, 30, 1, (1.0, 600, 1.3)),   # force-assigned chunks
+])
+def test_backward_multiprocess(L, tmp_path, P, pct, nhot, params):
+    """P processes on one GPU: dx, dgates on every rank; the native rank's weight gradients include
+    the partials its replicas computed and returned."""
+    from oracle import backward as O5
+    alpha, m, lam = params
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29800 + P + pct),
+               LLEP_TEST_PARAMS=f"{alpha},{m},{lam}", LLEP_TEST_BWD="1")
+    cmd = [sys.executable, os.path.join(HERE, "mp_layer_worker.py"), str(P), "tiny", str(pct), str(nhot), str(tmp_path)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = [np.load(os.path.join(tmp_path, f"rank{p}.npz")) for p in range(P)]
+    sh0 = W.CONFIGS["tiny"]
+    sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, P)
+    ws = LC.OracleWeights(sh.d_model, sh.d_ff, 21)
+    xs, ids, gs, dos = [], [], [], []
+    for p in range(P):
+        ids.append(W.routing_ids(sh, p, pct, nhot, 21))
+        gs.append(W.gate_weights(sh.tokens_per_rank, sh.top_k, p, 21).astype(np.float64))
+        xs.append(W.bf16_bits_to_f64(W.tokens_bits(sh.tokens_per_rank, sh.d_model, p, 21)))
+        dos.append(W.bf16_bits_to_f64(W.tokens_bits(sh.tokens_per_rank, sh.d_model, p + 1000, 21)))
+    dx, dg, dW, plan = O5.dispatch_combine_backward(xs, ids, gs, dos, ws, sh.n_experts, P, "llep", alpha, m, lam)
+    assert plan.transfers
+    M = sh.experts_per_rank
+    for p in range(P):
+        got = (res[p]["dx"], res[p]["dgates"], res[p]["dw13"], res[p]["dw2"])
+        _check_grads(sh, got, dx[p], dg[p], dW, range(p * M, (p + 1) * M), p * M)

@@ -105,3 +105,48 @@ def test_grouped_gemm(L, mode, kdim, nout, pair):
     for (e, rb, n) in groups:
         mask[rb:rb + n] = False
     assert out[mask].abs().max().item() == 0.0
+
+
+@pytest.mark.parametrize("kind,kdim,nout", [
+    (0, 2880, 2880),   # dA = dY · W_down   (W_down [D][H])
+    (0, 5760, 2880),   # dX = dGU · W13     (W13 [2H][D])
+    (0, 256, 512),
+    (1, 2880, 2880),   # dW_down = dYᵀ · a  (mdim = D, nout = H)
+    (1, 5760, 2880),   # dW13 = dGUᵀ · X    (mdim = 2H, nout = D)
+    (1, 512, 256),
+])
+def test_gemm_bwd(L, kind, kdim, nout):
+    """Backward GEMMs with MN-major UMMA operands vs a plain fp32 torch reference."""
+    g = torch.Generator(device="cuda").manual_seed(kind * 100 + kdim + nout)
+    E = 3
+    sizes = [1, 300, 129, 600, 256]
+    groups, rb = [], 0
+    for i, n in enumerate(sizes):
+        groups.append((i % E, rb, n))
+        rb += (n + 255) // 256 * 256
+    rows = rb
+    if kind == 0:
+        a = torch.randn((rows, kdim), generator=g, device="cuda").to(torch.bfloat16)
+        w = (torch.randn((E, kdim, nout), generator=g, device="cuda") / kdim ** 0.5).to(torch.bfloat16)
+        out = L.gemm_bwd(0, a, w, groups, nout, kdim, E)
+        torch.cuda.synchronize()
+        for (e, rb, n) in groups:
+            ref = a[rb:rb + n].float() @ w[e].float()
+            y = out[rb:rb + n].float()
+            err = ((y - ref).norm() / ref.norm()).item()
+            assert err < 5e-3 and (y - ref).abs().max().item() / ref.abs().max().item() < 2e-2, (e, n, err)
+    else:
+        mdim = kdim
+        a = torch.randn((rows, mdim), generator=g, device="cuda").to(torch.bfloat16)
+        b = torch.randn((rows, nout), generator=g, device="cuda").to(torch.bfloat16)
+        for (e, rb, n) in groups:  # zero the padding rows of each group
+            a[rb + n:rb + (n + 255) // 256 * 256] = 0
+            b[rb + n:rb + (n + 255) // 256 * 256] = 0
+        gl = [(i, rb, n) for i, (e, rb, n) in enumerate(groups)]
+        out = L.gemm_bwd(1, a, b, gl, nout, mdim, len(gl))
+        torch.cuda.synchronize()
+        for (i, rb, n) in gl:
+            ref = a[rb:rb + n].float().T @ b[rb:rb + n].float()
+            y = out[i]
+            err = ((y - ref).norm() / ref.norm()).item()
+            assert err < 1e-4, (i, n, err)

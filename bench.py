@@ -183,6 +183,36 @@ def run_mode(L, shape, rank, local, world, group, inputs, ep: bool, steps: int, 
     return res
 
 
+def run_backward(L, ctx, shape, inputs, steps, warmup, world, seed):
+    """Row f1: prepare + llep_moe_backward per step (recompute + all gradients), CUDA-event timed."""
+    import torch
+    x, ids, gates, w13, w2 = inputs
+    dout = W.tokens_torch(shape.tokens_per_rank, shape.d_model, 1000 + int(os.environ.get("RANK", "0")),
+                          x.device, seed)
+    ctx.enable_backward()
+    plan_buf = torch.empty(L.plan_bytes(shape.n_experts, world), dtype=torch.uint8, device=x.device)
+    dx = torch.empty_like(x)
+    dg = torch.empty(ids.shape, dtype=torch.float32, device=x.device)
+    M, D, H = shape.experts_per_rank, shape.d_model, shape.d_ff
+    dw13 = torch.empty((M, 2 * H, D), dtype=torch.float32, device=x.device)
+    dw2 = torch.empty((M, D, H), dtype=torch.float32, device=x.device)
+
+    def step():
+        plan, _ = ctx.prepare(ids, plan_out=plan_buf)
+        ctx.backward(x, ids, gates, dout, w13, w2, plan, dx, dg, dw13, dw2)
+
+    for _ in range(warmup):
+        step()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    barrier(world)
+    return max_over_ranks(e0.elapsed_time(e1), world) / steps
+
+
 def run_e2e(L, ctx, shape, host, dev, steps, warmup, world, ep=False):
     """Public API end to end: every step copies its inputs from pinned host memory (H2D), runs the
     layer (llep_prepare + llep_moe_forward) and reads the output back (D2H).  Double-buffered: the
@@ -330,6 +360,9 @@ def gpu_main(args):
                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
                "note": "pinned host -> device inputs and device -> host output every step, "
                        "double-buffered on copy streams"}
+    bwd_ms = None
+    if not args.no_backward:
+        bwd_ms = run_backward(L, ll_ctx, shape, inputs, max(3, args.steps // 2), 3, world, SEED)
     ll_ctx.close()
 
     sweep = []
@@ -406,6 +439,13 @@ def gpu_main(args):
         "gpu_launches": st["kernel_launches"],
         "clocks": ll["clocks"],
     }
+    if bwd_ms:
+        bwd_flops = 16.0 * D * H * rows_per_launch   # GU 4DH + dA 2DH + dW_down 2DH + dW13 4DH + dX 4DH
+        line["backward"] = {"ms_per_step": bwd_ms, "tokens_s": world * B / (bwd_ms / 1e3),
+                            "fwd_bwd_tokens_s": world * B / ((bwd_ms + step_ms) / 1e3),
+                            "tflops": bwd_flops / (bwd_ms / 1e3) / 1e12,
+                            "note": "llep_prepare + llep_moe_backward (recomputes the forward internals; "
+                                    "dx, dgates, dW13, dW_down incl. spilled-expert gradient return)"}
     if e2e:
         line["e2e"] = e2e
     if sweep:
@@ -481,6 +521,7 @@ def main():
     ap.add_argument("--mem-cap-gb", type=float, default=None,
                     help="per-GPU memory cap (the Q3 'tight memory cap' config): EP reports OOM if its plan does not fit")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-backward", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -18,7 +18,11 @@ def short(name):
     if not m:
         m = re.search(r"(grouped_gemm_2cta_kernel|grouped_gemm_kernel)<(?:\(int\))?(\d+), (?:\(int\))?(\d)>", name)
     if m:
-        return f"{m.group(1)}<{m.group(2)},{m.group(3)}> ({'GEMM1+SwiGLU' if m.group(3) == '0' else 'GEMM2+gate'})"
+        kind = {"0": "GEMM1+SwiGLU", "1": "GEMM2+gate", "2": "GEMM1 recompute, raw gate/up (backward)"}[m.group(3)]
+        return f"{m.group(1)}<{m.group(2)},{m.group(3)}> ({kind})"
+    m = re.search(r"gemm_bwd_kernelILi(\d)E", name) or re.search(r"gemm_bwd_kernel<(?:\(int\))?(\d)>", name)
+    if m:
+        return f"gemm_bwd_kernel<{m.group(1)}> ({'dY·W / dGU·W13 (MN-major B)' if m.group(1) == '0' else 'weight gradients (MN-major A, B)'})"
     m = re.search(r"([a-z_0-9]+_kernel)", name)
     return m.group(1) if m else name[:50]
 

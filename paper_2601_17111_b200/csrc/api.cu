@@ -210,6 +210,8 @@ struct llep_context {
   size_t off_o = 0, off_grad = 0;
   uint16_t *gu = nullptr, *da0 = nullptr, *aw = nullptr, *dgu = nullptr;
   float *stage13 = nullptr, *stage2 = nullptr;
+  float *wsbuf = nullptr;   // split-K partials of the weight-gradient GEMMs
+  int64_t ws_cap = 0;       // floats
   uint8_t *peer_base[kMaxWorld] = {};
   bool peer_opened[kMaxWorld] = {};
   bool peers_ready = false;
@@ -483,7 +485,7 @@ void llep_context_destroy(llep_context *c) {
   void *ptrs[] = {c->tile_cnt, c->tile_off, c->cnt, c->local_rank, c->slot_dst, c->err,
                   c->lm_local, c->rows_on, c->chunk_row, c->foreign_slot, c->dev_padded,
                   c->dev_foreign, c->groups, c->sched, c->summary, c->d_ptrs, c->act, c->arena,
-                  c->gu, c->da0, c->aw, c->dgu, c->stage13, c->stage2};
+                  c->gu, c->da0, c->aw, c->dgu, c->stage13, c->stage2, c->wsbuf};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->summary_host) cudaFreeHost(c->summary_host);
@@ -848,6 +850,34 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
 }
 
 
+// This rank's expert groups in the layout kernel's order (native with rows, then foreign, ascending
+// ids), from the host copy of the plan: rows, weight slot (>= 0 native, -1-f foreign), expert.
+static void my_groups_host(const llep_context *c, std::vector<int32_t> &rows, std::vector<int32_t> &wslot,
+                           std::vector<int32_t> &expert) {
+  const PlanLayout L = plan_layout(c->N, c->P);
+  const llep_chunk *chunks = reinterpret_cast<const llep_chunk *>(c->plan_host.data() + L.off_chunks);
+  const int32_t *n_chunks = reinterpret_cast<const int32_t *>(c->plan_host.data() + L.off_n_chunks);
+  rows.clear();
+  wslot.clear();
+  expert.clear();
+  int f = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int e = 0; e < c->N; ++e) {
+      const bool native = e / c->M == c->rank;
+      if (native != (pass == 0)) continue;
+      int r = 0;
+      for (int k = 0; k < n_chunks[e]; ++k) {
+        const llep_chunk ch = chunks[(size_t)e * (c->P + 1) + k];
+        if (ch.device == c->rank) r += ch.end - ch.start;
+      }
+      if (r == 0) continue;
+      rows.push_back(r);
+      wslot.push_back(native ? e - c->rank * c->M : -1 - f);
+      expert.push_back(e);
+      if (!native) ++f;
+    }
+}
+
 llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t *ids,
                               const float *topk_w, const uint16_t *dout, int64_t B,
                               const uint16_t *w13, const uint16_t *w2, const void *plan, uint16_t *dx,
@@ -964,30 +994,52 @@ llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t 
     // SwiGLU backward per row; dL/dw replaces the gate in G
     LLEP_CUDA(launch_bwd_swiglu(c->groups, G_, (int)sum.my_padded, H, c->gu, c->da0, G, c->aw, c->dgu, s));
     ++c->launches;
-    // dW_down = dOᵀ · (w a)   and   dW13 = [dg|du]ᵀ · X   (native -> dw2/dw13, foreign -> staging)
+    // dW_down = dOᵀ · (w a)   and   dW13 = [dg|du]ᵀ · X   (native -> dw2/dw13, foreign -> staging);
+    // large groups are split along their rows, partials summed in fixed order (deterministic)
+    std::vector<int32_t> grows, gslot, gexp;
+    my_groups_host(c, grows, gslot, gexp);
+    const int64_t need_ws = std::max(wgrad_workspace(grows.data(), (int)grows.size(), D, H, c->num_sms),
+                                     wgrad_workspace(grows.data(), (int)grows.size(), 2 * H, D, c->num_sms));
+    if (need_ws > c->ws_cap) {
+      LLEP_CUDA(cudaStreamSynchronize(s));
+      if (c->wsbuf) cudaFree(c->wsbuf);
+      c->wsbuf = nullptr;
+      c->ws_cap = 0;
+      LLEP_CUDA(cudaMalloc(&c->wsbuf, (size_t)need_ws * 4));
+      c->ws_cap = need_ws;
+    }
     BwdArgs w;
     memset(&w, 0, sizeof(w));
     w.kind = 1;
+    w.n_out_slots = M;
+    w.n_foreign_slots = c->arena_foreign;
     w.rows = c->arena_rows;
     w.kdim = 8;
     w.groups = c->groups;
     w.n_groups = G_;
     w.mblk_scale = 2;
     w.num_sms = c->num_sms;
+    w.ws = c->wsbuf;
     w.a = O;
     w.b = c->aw;
     w.mdim = D;
     w.nout = H;
+    w.n_ws_slots = c->ws_cap / ((int64_t)D * H);
     w.out = dw2;
     w.out_foreign = c->stage2;
     if ((st = run_gemm_bwd(w, s)) != LLEP_OK) return st;
+    if ((st = reduce_wgrad_splits(w, grows.data(), gslot.data(), gexp.data(), (int)grows.size(), s)) != LLEP_OK)
+      return st;
     w.a = c->dgu;
     w.b = X;
     w.mdim = 2 * H;
     w.nout = D;
+    w.n_ws_slots = c->ws_cap / ((int64_t)2 * H * D);
     w.out = dw13;
     w.out_foreign = c->stage13;
     if ((st = run_gemm_bwd(w, s)) != LLEP_OK) return st;
+    if ((st = reduce_wgrad_splits(w, grows.data(), gslot.data(), gexp.data(), (int)grows.size(), s)) != LLEP_OK)
+      return st;
     c->launches += 2;
     // dX = [dg|du] · W13   (W13 [2H][D] row-major: MN-major B), into X's rows (X is dead now)
     b.a = c->dgu;
@@ -1210,7 +1262,23 @@ llep_status llep_gemm_bwd(int32_t kind, const uint16_t *a, const uint16_t *w_or_
   ba.mblk_scale = 2;   // Group.mblk_start counts 256-row blocks
   ba.out = out;
   ba.num_sms = sms;
+  std::vector<int32_t> nr(n_groups), ex(n_groups);
+  for (int i = 0; i < n_groups; ++i) {
+    nr[i] = groups[4 * i + 2];
+    ex[i] = groups[4 * i];
+  }
+  float *ws = nullptr;
+  if (kind == 1) {
+    const int64_t need = wgrad_workspace(nr.data(), n_groups, ba.mdim, nout, sms);
+    if (need > 0) LLEP_CUDA(cudaMallocAsync(&ws, (size_t)need * 4, s));
+    ba.n_ws_slots = need / ((int64_t)ba.mdim * nout);
+    ba.n_out_slots = n_weights;
+  }
+  ba.ws = ws;
   llep_status st = n_groups > 0 ? run_gemm_bwd(ba, s) : LLEP_OK;
+  if (st == LLEP_OK && kind == 1 && n_groups > 0)
+    st = reduce_wgrad_splits(ba, nr.data(), nr.data(), ex.data(), n_groups, s);
+  if (ws) cudaFreeAsync(ws, s);
   cudaFreeAsync(dg, s);
   return st;
 }

@@ -64,6 +64,25 @@ __host__ __device__ inline int64_t interleave_pos(bool big, int64_t idx, int64_t
 }
 __host__ __device__ inline int32_t sched_pack(int32_t g, int32_t m) { return (g << 20) | m; }
 
+// Split-K of the weight-gradient GEMMs (contraction over a group's rows): a group with many rows is
+// cut into K ranges so its output tiles fill the SMs in several waves; each range writes an fp32
+// partial into a workspace and the partials are summed in fixed order (deterministic).
+constexpr int kSplitMinRows = 4096;
+__host__ __device__ inline int wgrad_splits(int n_rows, int tiles_per_split, int num_sms) {
+  const int padded = (n_rows + 255) / 256 * 256;
+  if (n_rows < kSplitMinRows) return 1;
+  int want = (4 * num_sms + tiles_per_split - 1) / tiles_per_split;   // >= ~4 waves per group
+  const int cap = padded / 1024;                                       // >= 1024 rows per split
+  if (want > cap) want = cap;
+  if (want < 1) want = 1;
+  const int ks = ((padded + want - 1) / want + 255) / 256 * 256;       // 256-row aligned K range
+  return (padded + ks - 1) / ks;
+}
+__host__ __device__ inline int wgrad_split_rows(int n_rows, int splits) {
+  const int padded = (n_rows + 255) / 256 * 256;
+  return ((padded + splits - 1) / splits + 255) / 256 * 256;
+}
+
 // Group table entry (8 int32) of one expert group a device computes.
 struct Group {
   int32_t expert;      // global expert id
@@ -193,6 +212,8 @@ struct BwdArgs {
   int32_t n_foreign;
   void *out_foreign;          // kind 1: output of groups with wslot < 0 (slot -1 - wslot); nullptr:
                               // every group writes `out` at slot Group.expert
+  float *ws;                  // kind 1: split-K partials (wgrad_workspace floats)
+  int64_t n_out_slots, n_foreign_slots, n_ws_slots;  // kind 1: [mdim x nout] slots behind each
   const Group *groups;
   int32_t n_groups;
   int32_t mblk_scale;
@@ -200,5 +221,9 @@ struct BwdArgs {
   int32_t num_sms;
 };
 llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s);
+// host: workspace floats of a kind-1 launch over groups with these row counts; reduce the partials
+int64_t wgrad_workspace(const int32_t *n_rows, int n_groups, int mdim, int nout, int num_sms);
+llep_status reduce_wgrad_splits(const BwdArgs &a, const int32_t *n_rows, const int32_t *wslots,
+                                const int32_t *experts, int n_groups, cudaStream_t s);
 
 }  // namespace llep

@@ -754,11 +754,16 @@ constexpr int kBwdBN = 256;
 constexpr int kBwdA = BM * BK * 2;        // 16 KB (K-major 128 rows, or 2 MN chunks)
 constexpr int kBwdB = kBwdBN * BK * 2;    // 32 KB (4 MN chunks)
 constexpr int kBwdStage = kBwdA + kBwdB;
-constexpr int kBwdStages = 4;
-constexpr int kBwdSmem = kBwdStages * kBwdStage + 1024 + 256;
+constexpr int kBwdStg = BM * 32 * 4;   // KIND 1 epilogue staging buffer: [128 rows][32 fp32]
+constexpr int kBwdNStg = 4;            // KIND 1: staging buffers (stores in flight)
+template <int KIND> struct BwdCfg {
+  static constexpr int STAGES = KIND == 0 ? 4 : 3;
+  static constexpr int SMEM = STAGES * kBwdStage + 1024 + (KIND == 1 ? kBwdNStg * kBwdStg : 0) + 1024;
+};
 
 struct BwdParams {
   CUtensorMap tmA, tmB, tmB1;   // tmB1: foreign-expert weights (KIND 0, groups with wslot < 0)
+  CUtensorMap tmO, tmOF, tmWS;  // KIND 1 fp32 outputs, 3D {nout, mdim, slot}: out, out_foreign, ws
   const Group *groups;
   int32_t n_groups;
   int32_t kdim;          // KIND 0: contraction length (rows of W_e)
@@ -768,6 +773,8 @@ struct BwdParams {
   int32_t mblk_scale;    // KIND 0: 128-row blocks per Group.mblk_start unit
   void *out;
   void *out_foreign;     // KIND 1: output of foreign groups (wslot < 0), nullptr -> out[expert]
+  float *ws;             // KIND 1: split-K partials
+  int32_t num_sms;
 };
 
 __device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr) {
@@ -781,7 +788,7 @@ __device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr) {
 }
 
 struct BwdTile {
-  int row0, row_end, m0, n0, g, nk;
+  int row0, row_end, m0, n0, g, nk, split, nsplit;
 };
 
 template <int KIND>
@@ -803,23 +810,38 @@ __device__ __forceinline__ BwdTile decode_bwd(int t, const BwdParams &p, const i
     ti.m0 = 0;
     ti.nk = (p.kdim + BK - 1) / BK;
   } else {
+    // s_mblk holds, in schedule order (split groups first), the first tile of each entry; the
+    // group id of entry i is s_mblk[kMaxGroups / 2 + i] (KIND 1 uses two half-size arrays)
     const int per = p.n_mt * p.n_nt;
-    ti.g = t / per;
-    const int r = t - ti.g * per;
+    int lo = 0, hi = p.n_groups - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_mblk[mid] <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    ti.g = s_mblk[kMaxGroups / 2 + lo];
+    const int rel = t - s_mblk[lo];
+    ti.split = rel / per;
+    const int r = rel - ti.split * per;
     const int mt = r / p.n_nt;
     ti.m0 = mt * BM;
     ti.n0 = (r - mt * p.n_nt) * kBwdBN;
     const Group g = p.groups[ti.g];
-    ti.row0 = g.row_base;
+    ti.nsplit = wgrad_splits(g.n_rows, per, p.num_sms);
+    const int ks = wgrad_split_rows(g.n_rows, ti.nsplit);
+    const int padded = (g.n_rows + 255) / 256 * 256;
+    const int k0 = ti.split * ks;
+    const int k1 = min(padded, k0 + ks);
+    ti.row0 = g.row_base + k0;
     ti.row_end = g.row_base + g.n_rows;
-    ti.nk = (g.n_rows + 255) / 256 * (256 / BK);   // padded rows are zero in both operands
+    ti.nk = (k1 - k0) / BK;     // padded rows are zero in both operands
   }
   return ti;
 }
 
 template <int KIND>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_kernel(const __grid_constant__ BwdParams p) {
-  constexpr int S = kBwdStages;
+  constexpr int S = BwdCfg<KIND>::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -828,9 +850,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_kernel(const __grid_
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S * kBwdStage);
   uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
-  __shared__ int s_mblk[kMaxGroups];
+  float *stg = reinterpret_cast<float *>(smem + S * kBwdStage + 1024);
+  int ep_chunk = 0;
+  __shared__ int s_mblk[kMaxGroups + 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int g = threadIdx.x; g < p.n_groups; g += kGemmThreads) s_mblk[g] = p.groups[g].mblk_start;
+  int total_tiles_k1 = 0;
+  if (KIND == 0) {
+    for (int g = threadIdx.x; g < p.n_groups; g += kGemmThreads) s_mblk[g] = p.groups[g].mblk_start;
+  } else if (threadIdx.x == 0) {
+    // schedule order: split groups (their many K-ranges) first, then the others
+    const int per = p.n_mt * p.n_nt;
+    int pos = 0, tile = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int g = 0; g < p.n_groups; ++g) {
+        const int ns = wgrad_splits(p.groups[g].n_rows, per, p.num_sms);
+        if ((ns > 1) != (pass == 0)) continue;
+        s_mblk[pos] = tile;
+        s_mblk[kMaxGroups / 2 + pos] = g;
+        ++pos;
+        tile += ns * per;
+      }
+    s_mblk[kMaxGroups / 2 - 1] = tile;
+  }
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(smem_u32(full + i), 1);
@@ -851,13 +892,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_kernel(const __grid_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  (void)total_tiles_k1;
   int total_tiles = 0;
   if (p.n_groups > 0) {
     if (KIND == 0) {
       const Group last = p.groups[p.n_groups - 1];
       total_tiles = (last.mblk_start * p.mblk_scale + (last.n_rows + BM - 1) / BM) * p.n_nt;
     } else {
-      total_tiles = p.n_groups * p.n_mt * p.n_nt;
+      total_tiles = s_mblk[kMaxGroups / 2 - 1];
     }
   }
   if (warp == 0) {
@@ -954,24 +996,50 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_kernel(const __grid_
           }
         }
       } else {
-        const int m = ti.m0 + q * 32 + lane;
-        const bool ok = m < p.mdim;
+        // fp32 gradient tile -> shared memory (rows of 32 floats, 128-byte swizzle) -> TMA bulk
+        // tensor stores of [128 rows x 32 cols] boxes (3D map: rows past mdim are clipped, not
+        // written into the next expert's slot)
         const Group gg = p.groups[ti.g];
-        float *obase = reinterpret_cast<float *>(p.out);
-        size_t slot = (size_t)gg.expert;
+        const CUtensorMap *om = &p.tmO;
+        int slot = gg.expert;
         if (p.out_foreign) {
-          slot = gg.wslot >= 0 ? (size_t)gg.wslot : (size_t)(-1 - gg.wslot);
-          if (gg.wslot < 0) obase = reinterpret_cast<float *>(p.out_foreign);
+          slot = gg.wslot >= 0 ? gg.wslot : -1 - gg.wslot;
+          if (gg.wslot < 0) om = &p.tmOF;
         }
-        float *orow = obase + (slot * p.mdim + m) * p.nout + ti.n0;
+        if (ti.nsplit > 1) {  // partial of K-range ti.split -> workspace (groups in order, splits)
+          int off = 0;
+          const int per = p.n_mt * p.n_nt;
+          for (int g2 = 0; g2 < ti.g; ++g2) {
+            const int ns = wgrad_splits(p.groups[g2].n_rows, per, p.num_sms);
+            if (ns > 1) off += ns;
+          }
+          om = &p.tmWS;
+          slot = off + ti.split;
+        }
+        const int r = q * 32 + lane;
+        const bool leader = threadIdx.x == 64;
 #pragma unroll 1
-        for (int j = 0; j < kBwdBN; j += 8) {
-          float v[8];
-          tmem_ld8(taddr + j, v);
+        for (int c = 0; c < kBwdBN / 32; ++c, ++ep_chunk) {
+          const int b = ep_chunk % kBwdNStg;
+          if (leader) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");  // kBwdNStg - 1
+          asm volatile("bar.sync 2, 128;" ::: "memory");
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) tmem_ld8(taddr + c * 32 + 8 * i, v + 8 * i);
           tmem_ld_wait();
-          if (ok && ti.n0 + j < p.nout) {
-            *reinterpret_cast<float4 *>(orow + j) = make_float4(v[0], v[1], v[2], v[3]);
-            *reinterpret_cast<float4 *>(orow + j + 4) = make_float4(v[4], v[5], v[6], v[7]);
+          float *rowp = stg + b * (BM * 32) + r * 32;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            *reinterpret_cast<float4 *>(rowp + ((i ^ (r & 7)) * 4)) =
+                make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("bar.sync 2, 128;" ::: "memory");
+          if (leader) {
+            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                         ::"l"(reinterpret_cast<uint64_t>(om)), "r"(ti.n0 + c * 32), "r"(ti.m0), "r"(slot),
+                         "r"(smem_u32(stg + b * (BM * 32)))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
       }
@@ -980,6 +1048,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_kernel(const __grid_
       if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
     }
   }
+  if (KIND == 1 && threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1003,6 +1072,63 @@ bool make_map_box(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, i
 
 }  // namespace
 
+static bool make_map_out3d(CUtensorMap *m, const void *ptr, int nout, int mdim, int64_t slots) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  if (slots < 1) slots = 1;
+  cuuint64_t dims[3] = {(cuuint64_t)nout, (cuuint64_t)mdim, (cuuint64_t)slots};
+  cuuint64_t strides[2] = {(cuuint64_t)nout * 4, (cuuint64_t)mdim * nout * 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)BM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int64_t wgrad_workspace(const int32_t *n_rows, int n_groups, int mdim, int nout, int num_sms) {
+  const int per = ((mdim + BM - 1) / BM) * ((nout + kBwdBN - 1) / kBwdBN);
+  int64_t n = 0;
+  for (int g = 0; g < n_groups; ++g) {
+    const int ns = wgrad_splits(n_rows[g], per, num_sms);
+    if (ns > 1) n += (int64_t)ns * mdim * nout;
+  }
+  return n;
+}
+
+__global__ void split_reduce_kernel(float *__restrict__ dst, const float *__restrict__ parts, int n_parts,
+                                    int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 acc = reinterpret_cast<const float4 *>(parts)[i];
+    for (int s = 1; s < n_parts; ++s) {
+      const float4 v = reinterpret_cast<const float4 *>(parts)[s * n4 + i];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    reinterpret_cast<float4 *>(dst)[i] = acc;
+  }
+}
+
+llep_status reduce_wgrad_splits(const BwdArgs &a, const int32_t *n_rows, const int32_t *wslots,
+                                const int32_t *experts, int n_groups, cudaStream_t s) {
+  const int per = ((a.mdim + BM - 1) / BM) * ((a.nout + kBwdBN - 1) / kBwdBN);
+  const int64_t mn = (int64_t)a.mdim * a.nout;
+  int64_t off = 0;
+  for (int g = 0; g < n_groups; ++g) {
+    const int ns = wgrad_splits(n_rows[g], per, a.num_sms);
+    if (ns <= 1) continue;
+    float *dst;
+    if (a.out_foreign) {
+      dst = wslots[g] >= 0 ? reinterpret_cast<float *>(a.out) + (int64_t)wslots[g] * mn
+                           : reinterpret_cast<float *>(a.out_foreign) + (int64_t)(-1 - wslots[g]) * mn;
+    } else {
+      dst = reinterpret_cast<float *>(a.out) + (int64_t)experts[g] * mn;
+    }
+    split_reduce_kernel<<<296, 256, 0, s>>>(dst, a.ws + off * mn, ns, mn / 4);
+    LLEP_CUDA(cudaGetLastError());
+    off += ns;
+  }
+  return LLEP_OK;
+}
+
 llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s) {
   if (a.nout % 8 || a.kdim % 8 || a.mdim % 8) {
     set_error("backward GEMM needs dims %% 8 == 0");
@@ -1020,6 +1146,8 @@ llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s) {
   p.mblk_scale = a.mblk_scale;
   p.out = a.out;
   p.out_foreign = a.out_foreign;
+  p.ws = a.ws;
+  p.num_sms = a.num_sms;
   bool ok;
   if (a.kind == 0) {
     ok = make_map_box(&p.tmA, a.a, a.rows, a.kdim, BK, BM) &&
@@ -1029,7 +1157,12 @@ llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s) {
   } else {
     ok = make_map_box(&p.tmA, a.a, a.rows, a.mdim, 64, BK) &&
          make_map_box(&p.tmB, a.b, a.rows, a.nout, 64, BK) &&
-         make_map_box(&p.tmB1, a.b, a.rows, a.nout, 64, BK);
+         make_map_box(&p.tmB1, a.b, a.rows, a.nout, 64, BK) &&
+         make_map_out3d(&p.tmO, a.out, a.nout, a.mdim, a.n_out_slots) &&
+         make_map_out3d(&p.tmOF, a.out_foreign ? a.out_foreign : a.out, a.nout, a.mdim,
+                        a.out_foreign ? a.n_foreign_slots : a.n_out_slots) &&
+         make_map_out3d(&p.tmWS, a.ws ? (const void *)a.ws : a.out, a.nout, a.mdim,
+                        a.ws ? a.n_ws_slots : a.n_out_slots);
   }
   if (!ok) {
     set_error("cuTensorMapEncodeTiled failed for a backward GEMM operand");
@@ -1037,12 +1170,16 @@ llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s) {
   }
   static bool attr[2] = {false, false};
   if (!attr[a.kind]) {
-    LLEP_CUDA(cudaFuncSetAttribute(a.kind == 0 ? gemm_bwd_kernel<0> : gemm_bwd_kernel<1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem));
+    if (a.kind == 0)
+      LLEP_CUDA(cudaFuncSetAttribute(gemm_bwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     BwdCfg<0>::SMEM));
+    else
+      LLEP_CUDA(cudaFuncSetAttribute(gemm_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     BwdCfg<1>::SMEM));
     attr[a.kind] = true;
   }
-  if (a.kind == 0) gemm_bwd_kernel<0><<<a.num_sms, kGemmThreads, kBwdSmem, s>>>(p);
-  else gemm_bwd_kernel<1><<<a.num_sms, kGemmThreads, kBwdSmem, s>>>(p);
+  if (a.kind == 0) gemm_bwd_kernel<0><<<a.num_sms, kGemmThreads, BwdCfg<0>::SMEM, s>>>(p);
+  else gemm_bwd_kernel<1><<<a.num_sms, kGemmThreads, BwdCfg<1>::SMEM, s>>>(p);
   LLEP_CUDA(cudaGetLastError());
   return LLEP_OK;
 }

@@ -119,7 +119,7 @@ def test_gemm_bwd(L, kind, kdim, nout):
     """Backward GEMMs with MN-major UMMA operands vs a plain fp32 torch reference."""
     g = torch.Generator(device="cuda").manual_seed(kind * 100 + kdim + nout)
     E = 3
-    sizes = [1, 300, 129, 600, 256]
+    sizes = [1, 300, 129, 600, 256] + ([9000] if kind == 1 else [])   # 9000 rows: split-K path
     groups, rb = [], 0
     for i, n in enumerate(sizes):
         groups.append((i % E, rb, n))

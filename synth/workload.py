@@ -50,6 +50,10 @@ CONFIGS = {
     "g20": LayerShape(32, 4, 2880, 2880, 16384, 8),
     "g120": LayerShape(128, 4, 2880, 2880, 32768, 8),
     "q3": LayerShape(128, 8, 2048, 768, 65536, 8),
+    # row f3: the paper's other layer shapes (F-models P:632-686, F-head P:19-101; 16K / 32K per GPU)
+    "dsv3": LayerShape(256, 8, 7168, 2048, 16384, 8),
+    "kimi": LayerShape(384, 8, 7168, 2048, 16384, 8),
+    "fhead": LayerShape(128, 4, 2048, 2048, 32768, 8),
 }
 
 

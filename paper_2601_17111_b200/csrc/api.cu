@@ -217,6 +217,7 @@ struct llep_context {
   bool peers_ready = false;
   void **d_ptrs = nullptr;  // device: flags[P], lm[P], x[P], g[P], o[P], grad[P]
   uint32_t epoch = 0;
+  uint32_t wepoch = 0;      // row f2: weight-flag epoch, one per forward call (same on every rank)
   // host copy of the last prepared plan
   std::vector<uint8_t> plan_host;
   const void *plan_dev_cached = nullptr;
@@ -252,7 +253,7 @@ static void collect(llep_context *c) {
 static void layout_offsets(llep_context *c, int64_t rows, int32_t foreign) {
   size_t off = 0;
   c->off_flags = off;
-  off += 256;
+  off += 4 * (kWeightFlag0 + kMaxGroups);
   c->off_lm = off;
   off = align8(off + sizeof(int32_t) * (size_t)c->P * c->N);
   off = (off + 1023) & ~size_t(1023);
@@ -710,7 +711,7 @@ llep_status llep_prepare(llep_context *c, const int32_t *ids, int64_t B, const l
 // a7: for every 𝒲 entry (e, rank -> d) copy W13_e and W2_e into foreign slot f of device d
 // (f = position of e among d's foreign experts, ascending id) on the side stream (copy engines).
 static llep_status push_weights(llep_context *c, const uint16_t *w13, const uint16_t *w2, cudaStream_t s,
-                                bool *any_copy) {
+                                bool *any_copy, uint32_t signal_epoch = 0) {
   const int N = c->N, P = c->P, M = c->M, D = c->D, H = c->H;
   const PlanLayout L = plan_layout(N, P);
   const uint8_t *replica = c->plan_host.data() + L.off_replica;
@@ -734,6 +735,11 @@ static llep_status push_weights(llep_context *c, const uint16_t *w13, const uint
         LLEP_CUDA(cudaMemcpyAsync(c->peer_base[d] + c->off_w2 + (size_t)f * w2_bytes,
                                   w2 + (size_t)el * D * H, w2_bytes, cudaMemcpyDeviceToDevice,
                                   c->side));
+        if (signal_epoch) {   // row f2: the slot's weights have landed once this runs
+          uint32_t *flag = reinterpret_cast<uint32_t *>(c->peer_base[d] + c->off_flags) + kWeightFlag0 + f;
+          LLEP_CUDA(launch_signal(flag, signal_epoch, c->side));
+          ++c->launches;
+        }
       }
       ++f;
     }
@@ -762,9 +768,11 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   }
   const int N = c->N, P = c->P, M = c->M, D = c->D, H = c->H;
   (void)H;
-  // a7: weight migration, pushed by the native device on a side stream (copy engines)
+  // a7: weight migration, pushed by the native device on a side stream (copy engines); row f2: each
+  // destination's GEMM waits for a foreign slot's flag only when it reaches that slot's tiles
   bool any_copy = false;
-  if ((st = push_weights(c, w13, w2, s, &any_copy)) != LLEP_OK) return st;
+  const uint32_t wepoch = ++c->wepoch;
+  if ((st = push_weights(c, w13, w2, s, &any_copy, wepoch)) != LLEP_OK) return st;
   mark(c, 4, s);
   if (any_copy) LLEP_CUDA(cudaEventRecord(c->ev_join, c->side));
   // a6: dispatch (gather-on-send into every destination's receive rows)
@@ -789,8 +797,7 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   da.peer_x2 = nullptr;
   LLEP_CUDA(launch_dispatch(da, s));
   c->launches += B > 0;
-  if (any_copy) LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
-  if ((st = barrier(c, s)) != LLEP_OK) return st;
+  if ((st = barrier(c, s)) != LLEP_OK) return st;   // dispatched rows landed (weights: flags)
   mark(c, 5, s);
   // a8: GEMM1 + SwiGLU   X [rows, D] -> A [rows, H]
   uint16_t *X = reinterpret_cast<uint16_t *>(c->arena + c->off_x);
@@ -810,6 +817,8 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   g1.n_groups_host = sum.my_groups;
   g1.gate = nullptr;
   g1.out = c->act;
+  g1.wflags = P > 1 ? reinterpret_cast<const uint32_t *>(c->arena + c->off_flags) + kWeightFlag0 : nullptr;
+  g1.wepoch = wepoch;
   g1.num_sms = c->num_sms;
   g1.row_align = c->row_align;
   if (sum.my_groups > 0 && (st = run_grouped_gemm(g1, s)) != LLEP_OK) return st;
@@ -841,6 +850,7 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   ca.slot_out = nullptr;
   LLEP_CUDA(launch_combine(ca, s));
   c->launches += B > 0;
+  if (any_copy) LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));   // keep the side stream joined
   mark(c, 8, s);
   if (c->timing) {
     c->pending = true;

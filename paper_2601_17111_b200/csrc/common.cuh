@@ -144,6 +144,8 @@ cudaError_t launch_bwd_swiglu(const Group *groups, int n_groups, int n_rows_tota
                               const uint16_t *dA0, float *gate_io, uint16_t *Aw, uint16_t *dGU, cudaStream_t s);
 cudaError_t launch_grad_reduce(float *dst, const float *base, int n_src, int64_t stride_floats, int64_t n_floats,
                                cudaStream_t s);
+cudaError_t launch_signal(uint32_t *flag, uint32_t v, cudaStream_t s);
+constexpr int kWeightFlag0 = 32;   // arena flag words: [0, 32) barrier, [32, 32 + kMaxGroups) weight slots
 cudaError_t launch_mirror(const void *plan, size_t plan_bytes, const void *summary, size_t sum_bytes,
                           const int32_t *err, void *host_plan, void *host_sum, int32_t *host_err,
                           cudaStream_t s);
@@ -194,6 +196,8 @@ struct GemmArgs {
   int32_t n_groups_host;
   const float *gate;         // [rows] (mode 1)
   uint16_t *out;             // [rows, nout]
+  const uint32_t *wflags;    // row f2: foreign slot f's weights landed when wflags[f] >= wepoch
+  uint32_t wepoch;           //         (nullptr: weights already resident)
   int32_t num_sms;
   int32_t row_align;         // 128: 1-CTA M=128 tiles; 256: 2-CTA (cta_group::2) M=256 tiles
 };

@@ -42,7 +42,21 @@ struct GemmParams {
   int32_t kdim, nout, wrows, n_ntiles, wup_off;
   const float *gate;
   __nv_bfloat16 *out;
+  const uint32_t *wflags;
+  uint32_t wepoch;
 };
+
+// Row f2: wait until foreign slot f's weights have landed (flag published by the native device
+// with release semantics after its copy-engine push), then order the TMA reads after it.
+__device__ __forceinline__ void wait_weights(const GemmParams &p, int wslot) {
+  if (wslot >= 0 || !p.wflags) return;
+  const uint32_t *f = p.wflags + (-1 - wslot);
+  uint32_t v;
+  do {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  } while ((int32_t)(v - p.wepoch) < 0);
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 template <int BN>
 struct Cfg {
@@ -235,6 +249,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
         const TileInfo ti = decode_tile(t, p.n_ntiles, s_mblk, n_groups, p.groups, p.sched);
         const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
         const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
+        wait_weights(p, ti.wslot);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const uint32_t fb = smem_u32(full + stage);
@@ -511,6 +526,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
         const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
         const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
         const int brow = MODE != 1 ? wbase + (int)crank * p.wup_off : wbase + (int)crank * BH;
+        wait_weights(p, ti.wslot);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const uint32_t fl = smem_u32(full + stage);
@@ -1195,6 +1211,8 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   memset(&prm, 0, sizeof(prm));
   prm.groups = g.groups;
   prm.sched = g.sched;
+  prm.wflags = g.wflags;
+  prm.wepoch = g.wepoch;
   prm.n_groups_dev = g.n_groups_dev;
   prm.n_groups_host = g.n_groups_host;
   prm.kdim = g.kdim;

@@ -378,6 +378,14 @@ __global__ void grad_reduce_kernel(float *__restrict__ dst, const float *__restr
   }
 }
 
+// Row f2: after the copy engine has written an expert's weights into a peer's foreign slot (same
+// stream, so the copy completed first), publish `v` in that peer's weight flag with release
+// semantics at system scope; the peer's GEMM producers acquire it before loading those weights.
+__global__ void signal_kernel(uint32_t *flag, uint32_t v) {
+  __threadfence_system();
+  st_release_sys(flag, v);
+}
+
 // ----------------------------------------------------------------------- host read-back
 // Copies the plan blob, the layout summary and the error flags into mapped pinned host memory
 // with plain stores (zero-copy), so the one host synchronisation of the layer never queues
@@ -413,6 +421,11 @@ cudaError_t launch_grad_reduce(float *dst, const float *base, int n_src, int64_t
                                cudaStream_t s) {
   if (n_src <= 0) return cudaSuccess;
   grad_reduce_kernel<<<296, 256, 0, s>>>(dst, base, n_src, stride_floats / 4, n_floats / 4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_signal(uint32_t *flag, uint32_t v, cudaStream_t s) {
+  signal_kernel<<<1, 1, 0, s>>>(flag, v);
   return cudaGetLastError();
 }
 

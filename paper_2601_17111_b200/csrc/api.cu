@@ -708,40 +708,66 @@ llep_status llep_prepare(llep_context *c, const int32_t *ids, int64_t B, const l
   return LLEP_OK;
 }
 
-// a7: for every 𝒲 entry (e, rank -> d) copy W13_e and W2_e into foreign slot f of device d
-// (f = position of e among d's foreign experts, ascending id) on the side stream (copy engines).
+// a7: weight migration as a binomial broadcast tree per expert.  Holders of expert e are
+// h_0 = native(e) followed by its replica devices in ascending order; holder i sends to holders
+// i + 2^t for every 2^t > i (h_0 to 1, 2, 4, ...), so the native device's egress is ceil(log2(k+1))
+// copies instead of k.  A replica forwards from its own foreign slot after waiting for that slot's
+// flag; every copy is followed by a release-signal of the destination slot's flag (epoch `ep`).
+// f(e, d) = position of e among d's foreign experts (ascending id).  Side stream, copy engines.
 static llep_status push_weights(llep_context *c, const uint16_t *w13, const uint16_t *w2, cudaStream_t s,
-                                bool *any_copy, uint32_t signal_epoch = 0) {
+                                bool *any_copy, uint32_t ep) {
   const int N = c->N, P = c->P, M = c->M, D = c->D, H = c->H;
   const PlanLayout L = plan_layout(N, P);
   const uint8_t *replica = c->plan_host.data() + L.off_replica;
   const size_t w13_bytes = (size_t)2 * H * D * 2, w2_bytes = (size_t)D * H * 2;
   *any_copy = false;
-  for (int d = 0; d < P && P > 1; ++d) {
-    if (d == c->rank) continue;
-    int f = 0;
-    for (int e = 0; e < N; ++e) {
-      if (!replica[(size_t)e * P + d]) continue;
-      if (e / M == c->rank) {
-        if (!*any_copy) {
-          LLEP_CUDA(cudaEventRecord(c->ev_fork, s));
-          LLEP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-          *any_copy = true;
-        }
-        const int el = e - c->rank * M;
-        LLEP_CUDA(cudaMemcpyAsync(c->peer_base[d] + c->off_w13 + (size_t)f * w13_bytes,
-                                  w13 + (size_t)el * 2 * H * D, w13_bytes, cudaMemcpyDeviceToDevice,
-                                  c->side));
-        LLEP_CUDA(cudaMemcpyAsync(c->peer_base[d] + c->off_w2 + (size_t)f * w2_bytes,
-                                  w2 + (size_t)el * D * H, w2_bytes, cudaMemcpyDeviceToDevice,
-                                  c->side));
-        if (signal_epoch) {   // row f2: the slot's weights have landed once this runs
-          uint32_t *flag = reinterpret_cast<uint32_t *>(c->peer_base[d] + c->off_flags) + kWeightFlag0 + f;
-          LLEP_CUDA(launch_signal(flag, signal_epoch, c->side));
-          ++c->launches;
-        }
-      }
-      ++f;
+  if (P == 1) return LLEP_OK;
+  std::vector<int> fslot((size_t)N * P, -1), cnt(P, 0);
+  for (int e = 0; e < N; ++e)
+    for (int d = 0; d < P; ++d)
+      if (replica[(size_t)e * P + d]) fslot[(size_t)e * P + d] = cnt[d]++;
+  std::vector<int> holders;
+  for (int e = 0; e < N; ++e) {
+    holders.assign(1, e / M);
+    for (int d = 0; d < P; ++d)
+      if (replica[(size_t)e * P + d]) holders.push_back(d);
+    const int k = (int)holders.size() - 1;
+    int me = -1;
+    for (int i = 0; i <= k; ++i)
+      if (holders[i] == c->rank) me = i;
+    if (k == 0 || me < 0) continue;
+    int hb = 0;                                   // highest power of two <= me (0 for the native)
+    while (me > 0 && (2 << hb) <= me) ++hb;
+    const int t0 = me == 0 ? 0 : hb + 1;
+    if (me + (1 << t0) > k) continue;             // a leaf of the tree
+    if (!*any_copy) {
+      LLEP_CUDA(cudaEventRecord(c->ev_fork, s));
+      LLEP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+      *any_copy = true;
+    }
+    const uint8_t *src13, *src2;
+    if (me == 0) {
+      const int el = e - c->rank * M;
+      src13 = reinterpret_cast<const uint8_t *>(w13 + (size_t)el * 2 * H * D);
+      src2 = reinterpret_cast<const uint8_t *>(w2 + (size_t)el * D * H);
+    } else {
+      const int f = fslot[(size_t)e * P + c->rank];
+      const uint32_t *own = reinterpret_cast<const uint32_t *>(c->arena + c->off_flags) + kWeightFlag0 + f;
+      LLEP_CUDA(launch_wait_flag(own, ep, c->err + 1, c->side));
+      ++c->launches;
+      src13 = c->arena + c->off_w13 + (size_t)f * w13_bytes;
+      src2 = c->arena + c->off_w2 + (size_t)f * w2_bytes;
+    }
+    for (int t = t0; me + (1 << t) <= k; ++t) {
+      const int d = holders[me + (1 << t)];
+      const int f = fslot[(size_t)e * P + d];
+      LLEP_CUDA(cudaMemcpyAsync(c->peer_base[d] + c->off_w13 + (size_t)f * w13_bytes, src13, w13_bytes,
+                                cudaMemcpyDeviceToDevice, c->side));
+      LLEP_CUDA(cudaMemcpyAsync(c->peer_base[d] + c->off_w2 + (size_t)f * w2_bytes, src2, w2_bytes,
+                                cudaMemcpyDeviceToDevice, c->side));
+      uint32_t *flag = reinterpret_cast<uint32_t *>(c->peer_base[d] + c->off_flags) + kWeightFlag0 + f;
+      LLEP_CUDA(launch_signal(flag, ep, c->side));
+      ++c->launches;
     }
   }
   return LLEP_OK;
@@ -922,7 +948,7 @@ llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t 
   float *G = reinterpret_cast<float *>(c->arena + c->off_g);
   // a7 + a6: weights to the replicas, x and dout rows + gates to their destinations
   bool any_copy = false;
-  if ((st = push_weights(c, w13, w2, s, &any_copy)) != LLEP_OK) return st;
+  if ((st = push_weights(c, w13, w2, s, &any_copy, ++c->wepoch)) != LLEP_OK) return st;
   if (any_copy) LLEP_CUDA(cudaEventRecord(c->ev_join, c->side));
   DispatchArgs da;
   da.x = x;

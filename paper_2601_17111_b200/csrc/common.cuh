@@ -145,6 +145,7 @@ cudaError_t launch_bwd_swiglu(const Group *groups, int n_groups, int n_rows_tota
 cudaError_t launch_grad_reduce(float *dst, const float *base, int n_src, int64_t stride_floats, int64_t n_floats,
                                cudaStream_t s);
 cudaError_t launch_signal(uint32_t *flag, uint32_t v, cudaStream_t s);
+cudaError_t launch_wait_flag(const uint32_t *flag, uint32_t v, int32_t *err, cudaStream_t s);
 constexpr int kWeightFlag0 = 32;   // arena flag words: [0, 32) barrier, [32, 32 + kMaxGroups) weight slots
 cudaError_t launch_mirror(const void *plan, size_t plan_bytes, const void *summary, size_t sum_bytes,
                           const int32_t *err, void *host_plan, void *host_sum, int32_t *host_err,

@@ -386,6 +386,19 @@ __global__ void signal_kernel(uint32_t *flag, uint32_t v) {
   st_release_sys(flag, v);
 }
 
+// Row f2 broadcast tree: a replica forwards an expert's weights only after its own copy landed.
+__global__ void wait_flag_kernel(const uint32_t *flag, uint32_t v, int32_t *err) {
+  const long long t0 = clock64();
+  long long spins = 0;
+  while ((int32_t)(ld_acquire_sys(flag) - v) < 0) {
+    if (((++spins) & 1023) == 0 && clock64() - t0 > 40000000000LL) {
+      atomicOr(err, 8);
+      break;
+    }
+  }
+  __threadfence_system();
+}
+
 // ----------------------------------------------------------------------- host read-back
 // Copies the plan blob, the layout summary and the error flags into mapped pinned host memory
 // with plain stores (zero-copy), so the one host synchronisation of the layer never queues
@@ -426,6 +439,11 @@ cudaError_t launch_grad_reduce(float *dst, const float *base, int n_src, int64_t
 
 cudaError_t launch_signal(uint32_t *flag, uint32_t v, cudaStream_t s) {
   signal_kernel<<<1, 1, 0, s>>>(flag, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_flag(const uint32_t *flag, uint32_t v, int32_t *err, cudaStream_t s) {
+  wait_flag_kernel<<<1, 1, 0, s>>>(flag, v, err);
   return cudaGetLastError();
 }
 

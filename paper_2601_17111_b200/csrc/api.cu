@@ -1025,6 +1025,7 @@ llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t 
     b.mblk_scale = 2;
     b.out = c->da0;
     b.num_sms = c->num_sms;
+    b.pair = getenv("LLEP_BWD_1CTA") ? 0 : 1;
     if ((st = run_gemm_bwd(b, s)) != LLEP_OK) return st;
     ++c->launches;
     // SwiGLU backward per row; dL/dw replaces the gate in G
@@ -1034,8 +1035,10 @@ llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t 
     // large groups are split along their rows, partials summed in fixed order (deterministic)
     std::vector<int32_t> grows, gslot, gexp;
     my_groups_host(c, grows, gslot, gexp);
-    const int64_t need_ws = std::max(wgrad_workspace(grows.data(), (int)grows.size(), D, H, c->num_sms),
-                                     wgrad_workspace(grows.data(), (int)grows.size(), 2 * H, D, c->num_sms));
+    const int bwd_pair = getenv("LLEP_BWD_1CTA") ? 0 : 1;   // 2-CTA backward GEMMs (A/B switch)
+    const int units = bwd_pair ? -(c->num_sms / 2) : c->num_sms;
+    const int64_t need_ws = std::max(wgrad_workspace(grows.data(), (int)grows.size(), D, H, units),
+                                     wgrad_workspace(grows.data(), (int)grows.size(), 2 * H, D, units));
     if (need_ws > c->ws_cap) {
       LLEP_CUDA(cudaStreamSynchronize(s));
       if (c->wsbuf) cudaFree(c->wsbuf);
@@ -1055,6 +1058,7 @@ llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t 
     w.n_groups = G_;
     w.mblk_scale = 2;
     w.num_sms = c->num_sms;
+    w.pair = bwd_pair;
     w.ws = c->wsbuf;
     w.a = O;
     w.b = c->aw;
@@ -1263,7 +1267,8 @@ llep_status llep_grouped_gemm(int32_t mode, const uint16_t *a, int64_t rows, int
 llep_status llep_gemm_bwd(int32_t kind, const uint16_t *a, const uint16_t *w_or_b, int64_t rows,
                           int32_t kdim_or_mdim, int32_t nout, int32_t n_weights, const int32_t *groups,
                           int32_t n_groups, void *out, void *stream) {
-  if (kind != 0 && kind != 1) return invalid("kind must be 0 or 1");
+  const int pair = (kind & 2) ? 1 : 0;   // kind bit 1: 2-CTA (cta_group::2) variant
+  kind &= 1;
   if (!a || !w_or_b || !groups || !out) return invalid("null pointer");
   if (n_groups < 0 || n_groups > kMaxGroups) return invalid("n_groups out of range");
   std::vector<Group> g(std::max(n_groups, 1));
@@ -1298,6 +1303,7 @@ llep_status llep_gemm_bwd(int32_t kind, const uint16_t *a, const uint16_t *w_or_
   ba.mblk_scale = 2;   // Group.mblk_start counts 256-row blocks
   ba.out = out;
   ba.num_sms = sms;
+  ba.pair = pair;
   std::vector<int32_t> nr(n_groups), ex(n_groups);
   for (int i = 0; i < n_groups; ++i) {
     nr[i] = groups[4 * i + 2];
@@ -1305,7 +1311,7 @@ llep_status llep_gemm_bwd(int32_t kind, const uint16_t *a, const uint16_t *w_or_
   }
   float *ws = nullptr;
   if (kind == 1) {
-    const int64_t need = wgrad_workspace(nr.data(), n_groups, ba.mdim, nout, sms);
+    const int64_t need = wgrad_workspace(nr.data(), n_groups, ba.mdim, nout, pair ? -(sms / 2) : sms);
     if (need > 0) LLEP_CUDA(cudaMallocAsync(&ws, (size_t)need * 4, s));
     ba.n_ws_slots = need / ((int64_t)ba.mdim * nout);
     ba.n_out_slots = n_weights;

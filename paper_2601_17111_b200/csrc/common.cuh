@@ -224,6 +224,7 @@ struct BwdArgs {
   int32_t mblk_scale;
   void *out;
   int32_t num_sms;
+  int32_t pair;               // 1: 2-CTA (cta_group::2) variant, 256-row / 256-output-row pair tiles
 };
 llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s);
 // host: workspace floats of a kind-1 launch over groups with these row counts; reduce the partials

@@ -790,7 +790,7 @@ struct BwdParams {
   void *out;
   void *out_foreign;     // KIND 1: output of foreign groups (wslot < 0), nullptr -> out[expert]
   float *ws;             // KIND 1: split-K partials
-  int32_t num_sms;
+  int32_t num_sms;       // scheduling units for the split heuristic (SMs, or CTA pairs)
 };
 
 __device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr) {
@@ -1073,6 +1073,284 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_kernel(const __grid_
                  "r"(2 * kAccCols) : "memory");
 }
 
+
+// ---------------------------------------------------------------- backward GEMMs, 2-CTA variant
+// Same two kinds on CTA pairs (cta_group::2): a pair tile is 256 rows (KIND 0) / 256 output rows
+// (KIND 1) x 256 columns; CTA r stages its 128 rows of A (K-major, or two 64-wide MN chunks) and
+// the r-th 128-column half of B (two MN chunks), the leader issues M=256 N=256 MMAs.
+constexpr int kPairA = BM * BK * 2;        // 16 KB per CTA
+constexpr int kPairB = 128 * BK * 2;       // 16 KB per CTA (half of N)
+constexpr int kPairStage = kPairA + kPairB;
+template <int KIND> struct BwdPairCfg {
+  static constexpr int STAGES = KIND == 0 ? 6 : 4;
+  static constexpr int SMEM = STAGES * kPairStage + 1024 + (KIND == 1 ? kBwdNStg * kBwdStg : 0) + 1024;
+};
+
+template <int KIND>
+__device__ __forceinline__ BwdTile decode_bwd_pair(int t, const BwdParams &p, const int *s_mblk) {
+  BwdTile ti;
+  if (KIND == 0) {
+    const int mb = t / p.n_nt;
+    ti.n0 = (t - mb * p.n_nt) * kBwdBN;
+    int lo = 0, hi = p.n_groups - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_mblk[mid] <= mb) lo = mid;
+      else hi = mid - 1;
+    }
+    const Group g = p.groups[lo];
+    ti.g = lo;
+    ti.row0 = g.row_base + (mb - s_mblk[lo]) * 2 * BM;
+    ti.row_end = g.row_base + g.n_rows;
+    ti.m0 = 0;
+    ti.nk = (p.kdim + BK - 1) / BK;
+  } else {
+    const int per = p.n_mt * p.n_nt;
+    int lo = 0, hi = p.n_groups - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_mblk[mid] <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    ti.g = s_mblk[kMaxGroups / 2 + lo];
+    const int rel = t - s_mblk[lo];
+    ti.split = rel / per;
+    const int r = rel - ti.split * per;
+    const int mt = r / p.n_nt;
+    ti.m0 = mt * 2 * BM;
+    ti.n0 = (r - mt * p.n_nt) * kBwdBN;
+    const Group g = p.groups[ti.g];
+    ti.nsplit = wgrad_splits(g.n_rows, per, p.num_sms);
+    const int ks = wgrad_split_rows(g.n_rows, ti.nsplit);
+    const int padded = (g.n_rows + 255) / 256 * 256;
+    const int k0 = ti.split * ks;
+    const int k1 = min(padded, k0 + ks);
+    ti.row0 = g.row_base + k0;
+    ti.row_end = g.row_base + g.n_rows;
+    ti.nk = (k1 - k0) / BK;
+  }
+  return ti;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __grid_constant__ BwdParams p) {
+  constexpr int S = BwdPairCfg<KIND>::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + S * kPairA;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S * kPairStage);
+  uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+  float *stg = reinterpret_cast<float *>(smem + S * kPairStage + 1024);
+  int ep_chunk = 0;
+  __shared__ int s_mblk[kMaxGroups + 2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  if (KIND == 0) {
+    for (int g = threadIdx.x; g < p.n_groups; g += kGemmThreads) s_mblk[g] = p.groups[g].mblk_start;
+  } else if (threadIdx.x == 0) {
+    const int per = p.n_mt * p.n_nt;
+    int pos = 0, tile = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int g = 0; g < p.n_groups; ++g) {
+        const int ns = wgrad_splits(p.groups[g].n_rows, per, p.num_sms);
+        if ((ns > 1) != (pass == 0)) continue;
+        s_mblk[pos] = tile;
+        s_mblk[kMaxGroups / 2 + pos] = g;
+        ++pos;
+        tile += ns * per;
+      }
+    s_mblk[kMaxGroups / 2 - 1] = tile;
+  }
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(smem_u32(full + i), 1);
+      mbar_init(smem_u32(empty + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(tfull + i), 1);
+      mbar_init(smem_u32(tempty + i), 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(2 * kAccCols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  int total_tiles = 0;
+  if (p.n_groups > 0) {
+    if (KIND == 0) {
+      const Group last = p.groups[p.n_groups - 1];
+      total_tiles = (last.mblk_start + (last.n_rows + 2 * BM - 1) / (2 * BM)) * p.n_nt;
+    } else {
+      total_tiles = s_mblk[kMaxGroups / 2 - 1];
+    }
+  }
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_normal();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < total_tiles; t += n_pairs) {
+        const BwdTile ti = decode_bwd_pair<KIND>(t, p, s_mblk);
+        const int ws = KIND == 0 ? p.groups[ti.g].wslot : 0;
+        const int wrow = (ws >= 0 ? ws : -1 - ws) * p.kdim;
+        const CUtensorMap *bm = (KIND == 0 && ws < 0) ? &p.tmB1 : &p.tmB;
+        for (int kb = 0; kb < ti.nk; ++kb) {
+          mbar_wait(smem_u32(empty + stage), phase ^ 1);
+          const uint32_t fl = smem_u32(full + stage);
+          if (leader) mbar_expect_tx(fl, 2 * kPairStage);
+          const uint32_t fb = mapa_shared(fl, 0);
+          const uint32_t a_dst = smem_u32(sA + stage * kPairA);
+          const uint32_t b_dst = smem_u32(sB + stage * kPairB);
+          if (KIND == 0) {
+            tma_load_2d_pair(a_dst, &p.tmA, fb, kb * BK, ti.row0 + (int)crank * BM, pol);
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              tma_load_2d_pair(b_dst + c * 8192, bm, fb, ti.n0 + (int)crank * 128 + c * 64, wrow + kb * BK, pol);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              tma_load_2d_pair(a_dst + c * 8192, &p.tmA, fb, ti.m0 + (int)crank * BM + c * 64, ti.row0 + kb * BK, pol);
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              tma_load_2d_pair(b_dst + c * 8192, &p.tmB, fb, ti.n0 + (int)crank * 128 + c * 64, ti.row0 + kb * BK, pol);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((KIND == 1 ? 1u : 0u) << 15) |
+                             (1u << 16) | ((uint32_t)(kBwdBN >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair; t < total_tiles; t += n_pairs, ++it) {
+        const BwdTile ti = decode_bwd_pair<KIND>(t, p, s_mblk);
+        const int acc = it & 1;
+        mbar_wait(smem_u32(tempty + acc), ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        for (int kb = 0; kb < ti.nk; ++kb) {
+          mbar_wait(smem_u32(full + stage), phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * kPairA);
+          const uint32_t b0 = smem_u32(sB + stage * kPairB);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = KIND == 0 ? smem_desc(a0 + kk * 32) : smem_desc_mn(a0 + kk * 2048);
+            tc_mma_pair(d_tmem, ad, smem_desc_mn(b0 + kk * 2048), idesc, (kb | kk) != 0);
+          }
+          tc_commit_pair(smem_u32(empty + stage));
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_pair(smem_u32(tfull + acc));
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    int it = 0;
+    for (int t = pair; t < total_tiles; t += n_pairs, ++it) {
+      const int acc = it & 1;
+      const BwdTile ti = decode_bwd_pair<KIND>(t, p, s_mblk);
+      mbar_wait(smem_u32(tfull + acc), (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
+      if (KIND == 0) {
+        const int row = ti.row0 + (int)crank * BM + q * 32 + lane;
+        const bool ok = row < ti.row_end;
+        __nv_bfloat16 *orow = reinterpret_cast<__nv_bfloat16 *>(p.out) + (size_t)row * p.nout + ti.n0;
+#pragma unroll 1
+        for (int j = 0; j < kBwdBN; j += 8) {
+          float v[8];
+          tmem_ld8(taddr + j, v);
+          tmem_ld_wait();
+          if (ok && ti.n0 + j < p.nout) {
+            uint4 o;
+            __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            *reinterpret_cast<uint4 *>(orow + j) = o;
+          }
+        }
+      } else {
+        const Group gg = p.groups[ti.g];
+        const CUtensorMap *om = &p.tmO;
+        int slot = gg.expert;
+        if (p.out_foreign) {
+          slot = gg.wslot >= 0 ? gg.wslot : -1 - gg.wslot;
+          if (gg.wslot < 0) om = &p.tmOF;
+        }
+        if (ti.nsplit > 1) {
+          int off = 0;
+          const int per = p.n_mt * p.n_nt;
+          for (int g2 = 0; g2 < ti.g; ++g2) {
+            const int ns = wgrad_splits(p.groups[g2].n_rows, per, p.num_sms);
+            if (ns > 1) off += ns;
+          }
+          om = &p.tmWS;
+          slot = off + ti.split;
+        }
+        const int r = q * 32 + lane;
+        const bool lead = threadIdx.x == 64;
+        const int m0 = ti.m0 + (int)crank * BM;
+#pragma unroll 1
+        for (int c = 0; c < kBwdBN / 32; ++c, ++ep_chunk) {
+          const int b = ep_chunk % kBwdNStg;
+          if (lead) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+          asm volatile("bar.sync 2, 128;" ::: "memory");
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) tmem_ld8(taddr + c * 32 + 8 * i, v + 8 * i);
+          tmem_ld_wait();
+          float *rowp = stg + b * (BM * 32) + r * 32;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            *reinterpret_cast<float4 *>(rowp + ((i ^ (r & 7)) * 4)) =
+                make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("bar.sync 2, 128;" ::: "memory");
+          if (lead) {
+            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                         ::"l"(reinterpret_cast<uint64_t>(om)), "r"(ti.n0 + c * 32), "r"(m0), "r"(slot),
+                         "r"(smem_u32(stg + b * (BM * 32)))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(tempty + acc), 0));
+    }
+  }
+  if (KIND == 1 && threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(2 * kAccCols) : "memory");
+}
+
 bool make_map_box(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, int box_cols, int box_rows) {
   auto enc = get_encode();
   if (!enc) return false;
@@ -1102,7 +1380,11 @@ static bool make_map_out3d(CUtensorMap *m, const void *ptr, int nout, int mdim, 
 }
 
 int64_t wgrad_workspace(const int32_t *n_rows, int n_groups, int mdim, int nout, int num_sms) {
-  const int per = ((mdim + BM - 1) / BM) * ((nout + kBwdBN - 1) / kBwdBN);
+  // num_sms > 0: 1-CTA tiles of 128 output rows over num_sms units; < 0: pair tiles of 256 rows
+  // over -num_sms units (CTA pairs)
+  const int tm = num_sms > 0 ? BM : 2 * BM;
+  num_sms = num_sms > 0 ? num_sms : -num_sms;
+  const int per = ((mdim + tm - 1) / tm) * ((nout + kBwdBN - 1) / kBwdBN);
   int64_t n = 0;
   for (int g = 0; g < n_groups; ++g) {
     const int ns = wgrad_splits(n_rows[g], per, num_sms);
@@ -1125,11 +1407,13 @@ __global__ void split_reduce_kernel(float *__restrict__ dst, const float *__rest
 
 llep_status reduce_wgrad_splits(const BwdArgs &a, const int32_t *n_rows, const int32_t *wslots,
                                 const int32_t *experts, int n_groups, cudaStream_t s) {
-  const int per = ((a.mdim + BM - 1) / BM) * ((a.nout + kBwdBN - 1) / kBwdBN);
+  const int tm = a.pair ? 2 * BM : BM;
+  const int units = a.pair ? a.num_sms / 2 : a.num_sms;
+  const int per = ((a.mdim + tm - 1) / tm) * ((a.nout + kBwdBN - 1) / kBwdBN);
   const int64_t mn = (int64_t)a.mdim * a.nout;
   int64_t off = 0;
   for (int g = 0; g < n_groups; ++g) {
-    const int ns = wgrad_splits(n_rows[g], per, a.num_sms);
+    const int ns = wgrad_splits(n_rows[g], per, units);
     if (ns <= 1) continue;
     float *dst;
     if (a.out_foreign) {
@@ -1158,12 +1442,12 @@ llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s) {
   p.mdim = a.mdim;
   p.nout = a.nout;
   p.n_nt = (a.nout + kBwdBN - 1) / kBwdBN;
-  p.n_mt = (a.mdim + BM - 1) / BM;
+  p.n_mt = (a.mdim + (a.pair ? 2 * BM : BM) - 1) / (a.pair ? 2 * BM : BM);
   p.mblk_scale = a.mblk_scale;
   p.out = a.out;
   p.out_foreign = a.out_foreign;
   p.ws = a.ws;
-  p.num_sms = a.num_sms;
+  p.num_sms = a.pair ? a.num_sms / 2 : a.num_sms;
   bool ok;
   if (a.kind == 0) {
     ok = make_map_box(&p.tmA, a.a, a.rows, a.kdim, BK, BM) &&
@@ -1183,6 +1467,29 @@ llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s) {
   if (!ok) {
     set_error("cuTensorMapEncodeTiled failed for a backward GEMM operand");
     return LLEP_ERR_CUDA;
+  }
+  if (a.pair) {
+    static bool pattr[2] = {false, false};
+    auto kern = a.kind == 0 ? gemm_bwd_pair_kernel<0> : gemm_bwd_pair_kernel<1>;
+    const int smem = a.kind == 0 ? BwdPairCfg<0>::SMEM : BwdPairCfg<1>::SMEM;
+    if (!pattr[a.kind]) {
+      LLEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      pattr[a.kind] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.num_sms & ~1));
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr2[1];
+    attr2[0].id = cudaLaunchAttributeClusterDimension;
+    attr2[0].val.clusterDim.x = 2;
+    attr2[0].val.clusterDim.y = 1;
+    attr2[0].val.clusterDim.z = 1;
+    cfg.attrs = attr2;
+    cfg.numAttrs = 1;
+    LLEP_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+    return LLEP_OK;
   }
   static bool attr[2] = {false, false};
   if (!attr[a.kind]) {

@@ -322,7 +322,7 @@ def grouped_gemm(mode: int, a, w, groups: Sequence[Tuple[int, int, int]], nout: 
 
 
 def gemm_bwd(kind: int, a, b, groups: Sequence[Tuple[int, int, int]], nout: int, kdim_or_mdim: int,
-             n_weights: int, out=None):
+             n_weights: int, out=None, pair: bool = False):
     """llep_gemm_bwd (see llep.h): kind 0 -> bf16 [rows, nout]; kind 1 -> fp32 [n_weights, mdim, nout]."""
     import torch
     rows = a.shape[0]
@@ -332,6 +332,6 @@ def gemm_bwd(kind: int, a, b, groups: Sequence[Tuple[int, int, int]], nout: int,
         else:
             out = torch.zeros((n_weights, kdim_or_mdim, nout), dtype=torch.float32, device=a.device)
     g = np.ascontiguousarray(np.asarray([[e, rb, n, 0] for (e, rb, n) in groups], dtype=np.int32).reshape(-1))
-    _check(_lib.llep_gemm_bwd(kind, a.data_ptr(), b.data_ptr(), rows, kdim_or_mdim, nout, n_weights,
+    _check(_lib.llep_gemm_bwd(kind | (2 if pair else 0), a.data_ptr(), b.data_ptr(), rows, kdim_or_mdim, nout, n_weights,
                               g.ctypes.data, len(groups), out.data_ptr(), _stream_ptr()))
     return out

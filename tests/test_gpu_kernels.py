@@ -107,6 +107,7 @@ def test_grouped_gemm(L, mode, kdim, nout, pair):
     assert out[mask].abs().max().item() == 0.0
 
 
+@pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("kind,kdim,nout", [
     (0, 2880, 2880),   # dA = dY · W_down   (W_down [D][H])
     (0, 5760, 2880),   # dX = dGU · W13     (W13 [2H][D])
@@ -115,7 +116,7 @@ def test_grouped_gemm(L, mode, kdim, nout, pair):
     (1, 5760, 2880),   # dW13 = dGUᵀ · X    (mdim = 2H, nout = D)
     (1, 512, 256),
 ])
-def test_gemm_bwd(L, kind, kdim, nout):
+def test_gemm_bwd(L, kind, kdim, nout, pair):
     """Backward GEMMs with MN-major UMMA operands vs a plain fp32 torch reference."""
     g = torch.Generator(device="cuda").manual_seed(kind * 100 + kdim + nout)
     E = 3
@@ -128,7 +129,7 @@ def test_gemm_bwd(L, kind, kdim, nout):
     if kind == 0:
         a = torch.randn((rows, kdim), generator=g, device="cuda").to(torch.bfloat16)
         w = (torch.randn((E, kdim, nout), generator=g, device="cuda") / kdim ** 0.5).to(torch.bfloat16)
-        out = L.gemm_bwd(0, a, w, groups, nout, kdim, E)
+        out = L.gemm_bwd(0, a, w, groups, nout, kdim, E, pair=pair)
         torch.cuda.synchronize()
         for (e, rb, n) in groups:
             ref = a[rb:rb + n].float() @ w[e].float()
@@ -143,7 +144,7 @@ def test_gemm_bwd(L, kind, kdim, nout):
             a[rb + n:rb + (n + 255) // 256 * 256] = 0
             b[rb + n:rb + (n + 255) // 256 * 256] = 0
         gl = [(i, rb, n) for i, (e, rb, n) in enumerate(groups)]
-        out = L.gemm_bwd(1, a, b, gl, nout, mdim, len(gl))
+        out = L.gemm_bwd(1, a, b, gl, nout, mdim, len(gl), pair=pair)
         torch.cuda.synchronize()
         for (i, rb, n) in gl:
             ref = a[rb:rb + n].float().T @ b[rb:rb + n].float()

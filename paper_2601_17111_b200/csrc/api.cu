@@ -204,6 +204,7 @@ struct llep_context {
   int64_t arena_rows = 0;
   int32_t arena_foreign = 0;
   size_t off_flags = 0, off_lm = 0, off_x = 0, off_g = 0, off_w13 = 0, off_w2 = 0;
+  size_t off_rsrc = 0, off_slot = 0;   // receive-row sources; slot buffer [max_tokens*K, D] (last)
   // backward (row f1): arena regions O [R, D] bf16 + returned weight-gradient slots, local buffers
   bool backward = false;
   int32_t arena_grad = 0;
@@ -263,6 +264,9 @@ static void layout_offsets(llep_context *c, int64_t rows, int32_t foreign) {
   c->off_g = off;
   off += (size_t)rows * 4;
   off = (off + 1023) & ~size_t(1023);
+  c->off_rsrc = off;
+  off += (size_t)rows * 4;
+  off = (off + 1023) & ~size_t(1023);
   c->off_w13 = off;
   off += (size_t)foreign * 2 * c->H * c->D * 2;
   off = (off + 1023) & ~size_t(1023);
@@ -274,6 +278,9 @@ static void layout_offsets(llep_context *c, int64_t rows, int32_t foreign) {
   off = (off + 1023) & ~size_t(1023);
   c->off_grad = off;
   if (c->backward) off += (size_t)c->arena_grad * 3 * c->H * c->D * 4;
+  off = (off + 1023) & ~size_t(1023);
+  c->off_slot = off;   // last: its size (this rank's max_tokens) may differ between ranks
+  off += (size_t)std::max<int64_t>(c->max_tokens, 1) * c->K * c->D * 2;
   c->arena_bytes = (off + 4095) & ~size_t(4095);
 }
 
@@ -292,7 +299,7 @@ static void close_peers(llep_context *c) {
 }
 
 static llep_status upload_peer_ptrs(llep_context *c) {
-  std::vector<void *> h(6 * c->P);
+  std::vector<void *> h(8 * c->P);
   for (int q = 0; q < c->P; ++q) {
     uint8_t *b = c->peer_base[q];
     h[q] = b + c->off_flags;
@@ -301,8 +308,10 @@ static llep_status upload_peer_ptrs(llep_context *c) {
     h[3 * c->P + q] = b + c->off_g;
     h[4 * c->P + q] = b + c->off_o;
     h[5 * c->P + q] = b + c->off_grad;
+    h[6 * c->P + q] = b + c->off_rsrc;
+    h[7 * c->P + q] = b + c->off_slot;
   }
-  LLEP_CUDA(cudaMemcpy(c->d_ptrs, h.data(), sizeof(void *) * 6 * c->P, cudaMemcpyHostToDevice));
+  LLEP_CUDA(cudaMemcpy(c->d_ptrs, h.data(), sizeof(void *) * 8 * c->P, cudaMemcpyHostToDevice));
   return LLEP_OK;
 }
 
@@ -312,6 +321,7 @@ static llep_status alloc_arena(llep_context *c, int64_t rows, int32_t foreign) {
   if (c->mem_cap > 0) {
     llep_context probe_sizes;  // offsets only
     probe_sizes.N = c->N; probe_sizes.D = c->D; probe_sizes.H = c->H; probe_sizes.P = c->P;
+    probe_sizes.K = c->K; probe_sizes.max_tokens = c->max_tokens;
     layout_offsets(&probe_sizes, rows, foreign);
     probe_sizes.backward = c->backward;
     probe_sizes.arena_grad = c->arena_grad;
@@ -455,7 +465,7 @@ llep_status llep_context_create(const llep_shape *s, int32_t rank, int32_t devic
   c->sched_cap = ((int64_t)P * slots + kRowAlign - 1) / kRowAlign + kMaxGroups;
   if (!e) e = A(&c->sched, sizeof(int32_t) * c->sched_cap);
   if (!e) e = A(&c->summary, sizeof(LayoutSummary));
-  if (!e) e = A(&c->d_ptrs, sizeof(void *) * 6 * P);
+  if (!e) e = A(&c->d_ptrs, sizeof(void *) * 8 * P);
   if (!e) e = cudaMemset(c->err, 0, sizeof(int32_t) * 4);
   if (!e) e = cudaHostAlloc(&c->summary_host, sizeof(LayoutSummary), cudaHostAllocMapped);
   if (!e) e = cudaHostAlloc(&c->err_host, sizeof(int32_t) * 4, cudaHostAllocMapped);
@@ -821,6 +831,7 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   da.slot_dst = c->slot_dst;
   da.x2 = nullptr;
   da.peer_x2 = nullptr;
+  da.peer_rsrc = reinterpret_cast<int32_t *const *>(c->d_ptrs + 6 * P);
   LLEP_CUDA(launch_dispatch(da, s));
   c->launches += B > 0;
   if ((st = barrier(c, s)) != LLEP_OK) return st;   // dispatched rows landed (weights: flags)
@@ -828,6 +839,7 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   // a8: GEMM1 + SwiGLU   X [rows, D] -> A [rows, H]
   uint16_t *X = reinterpret_cast<uint16_t *>(c->arena + c->off_x);
   GemmArgs g1;
+  memset(&g1, 0, sizeof(g1));
   g1.mode = 0;
   g1.a = X;
   g1.a_rows = c->arena_rows;
@@ -845,6 +857,8 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   g1.out = c->act;
   g1.wflags = P > 1 ? reinterpret_cast<const uint32_t *>(c->arena + c->off_flags) + kWeightFlag0 : nullptr;
   g1.wepoch = wepoch;
+  g1.row_src = nullptr;
+  g1.peer_slot = nullptr;
   g1.num_sms = c->num_sms;
   g1.row_align = c->row_align;
   if (sum.my_groups > 0 && (st = run_grouped_gemm(g1, s)) != LLEP_OK) return st;
@@ -860,21 +874,17 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   g2.nout = D;
   g2.gate = reinterpret_cast<const float *>(c->arena + c->off_g);
   g2.out = X;
+  // a9 + a10 fused: the epilogue pushes each gated row into its home rank's slot buffer (NVLink
+  // peer stores for remote rows, overlapped with the MMAs of later tiles)
+  g2.row_src = reinterpret_cast<const int32_t *>(c->arena + c->off_rsrc);
+  g2.peer_slot = reinterpret_cast<uint16_t *const *>(c->d_ptrs + 7 * P);
   if (sum.my_groups > 0 && (st = run_grouped_gemm(g2, s)) != LLEP_OK) return st;
   c->launches += sum.my_groups > 0;
   mark(c, 7, s);
   if ((st = barrier(c, s)) != LLEP_OK) return st;
-  // a10: combine (pull each slot's Y row from its device, K-sum in slot order)
-  CombineArgs ca;
-  ca.slot_dst = c->slot_dst;
-  ca.peer_y = peer_x(c);
-  ca.B = B;
-  ca.K = c->K;
-  ca.D = D;
-  ca.out = out;
-  ca.peer_s = nullptr;
-  ca.slot_out = nullptr;
-  LLEP_CUDA(launch_combine(ca, s));
+  // a10: local K-sum of the slot buffer the GEMM2 epilogues (this rank's and every peer's) filled
+  LLEP_CUDA(launch_combine_local(reinterpret_cast<const uint16_t *>(c->arena + c->off_slot), B, c->K, D,
+                                 c->slot_dst, out, s));
   c->launches += B > 0;
   if (any_copy) LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));   // keep the side stream joined
   mark(c, 8, s);
@@ -969,6 +979,7 @@ llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t 
   da.slot_dst = c->slot_dst;
   da.x2 = dout;
   da.peer_x2 = reinterpret_cast<uint16_t *const *>(c->d_ptrs + 4 * P);
+  da.peer_rsrc = nullptr;
   LLEP_CUDA(launch_dispatch(da, s));
   c->launches += B > 0;
   if (any_copy) LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
@@ -1241,6 +1252,7 @@ llep_status llep_grouped_gemm(int32_t mode, const uint16_t *a, int64_t rows, int
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   GemmArgs ga;
+  memset(&ga, 0, sizeof(ga));
   ga.mode = mode;
   ga.a = a;
   ga.a_rows = rows;

@@ -147,6 +147,8 @@ cudaError_t launch_grad_reduce(float *dst, const float *base, int n_src, int64_t
 cudaError_t launch_signal(uint32_t *flag, uint32_t v, cudaStream_t s);
 cudaError_t launch_wait_flag(const uint32_t *flag, uint32_t v, int32_t *err, cudaStream_t s);
 constexpr int kWeightFlag0 = 32;   // arena flag words: [0, 32) barrier, [32, 32 + kMaxGroups) weight slots
+cudaError_t launch_combine_local(const uint16_t *slotbuf, int64_t B, int K, int D, const int32_t *slot_dst,
+                                 uint16_t *out, cudaStream_t s);
 cudaError_t launch_mirror(const void *plan, size_t plan_bytes, const void *summary, size_t sum_bytes,
                           const int32_t *err, void *host_plan, void *host_sum, int32_t *host_err,
                           cudaStream_t s);
@@ -166,6 +168,7 @@ struct DispatchArgs {
   int32_t *slot_dst;        // [2*B*K] (device, row)
   const uint16_t *x2;       // optional second row source (backward: the upstream gradient dOut)
   uint16_t *const *peer_x2; // [P] its receive rows
+  int32_t *const *peer_rsrc;  // optional [P] per receive row: (flat slot << 5) | source rank
 };
 cudaError_t launch_dispatch(const DispatchArgs &a, cudaStream_t s);
 
@@ -199,6 +202,9 @@ struct GemmArgs {
   uint16_t *out;             // [rows, nout]
   const uint32_t *wflags;    // row f2: foreign slot f's weights landed when wflags[f] >= wepoch
   uint32_t wepoch;           //         (nullptr: weights already resident)
+  const int32_t *row_src;    // mode 1 push epilogue: (slot << 5) | rank of each receive row, and
+  uint16_t *const *peer_slot;//   [P] slot buffers [B*K, nout]: the row's output goes to
+                             //   peer_slot[rank] + slot*nout (nullptr: write `out` rows)
   int32_t num_sms;
   int32_t row_align;         // 128: 1-CTA M=128 tiles; 256: 2-CTA (cta_group::2) M=256 tiles
 };

@@ -44,6 +44,8 @@ struct GemmParams {
   __nv_bfloat16 *out;
   const uint32_t *wflags;
   uint32_t wepoch;
+  const int32_t *row_src;
+  uint16_t *const *peer_slot;
 };
 
 // Row f2: wait until foreign slot f's weights have landed (flag published by the native device
@@ -359,6 +361,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
       } else {
         const float gs = row_ok ? p.gate[row] : 0.f;
         __nv_bfloat16 *orow = p.out + (size_t)row * p.nout + col0;
+        if (p.peer_slot && row_ok) {  // fused combine push: this row's output -> its home slot
+          const int32_t src = p.row_src[row];
+          orow = reinterpret_cast<__nv_bfloat16 *>(p.peer_slot[src & 31]) + (size_t)(src >> 5) * p.nout + col0;
+        }
 #pragma unroll 1
         for (int j = 0; j < BNO; j += 8) {
           float v[8];
@@ -634,6 +640,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       } else {
         const float gs = row_ok ? p.gate[row] : 0.f;
         __nv_bfloat16 *orow = p.out + (size_t)row * p.nout + col0;
+        if (p.peer_slot && row_ok) {  // fused combine push: this row's output -> its home slot
+          const int32_t src = p.row_src[row];
+          orow = reinterpret_cast<__nv_bfloat16 *>(p.peer_slot[src & 31]) + (size_t)(src >> 5) * p.nout + col0;
+        }
 #pragma unroll 1
         for (int j = 0; j < BNO; j += 8) {
           float v[8];
@@ -1520,6 +1530,8 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   prm.sched = g.sched;
   prm.wflags = g.wflags;
   prm.wepoch = g.wepoch;
+  prm.row_src = g.row_src;
+  prm.peer_slot = g.peer_slot;
   prm.n_groups_dev = g.n_groups_dev;
   prm.n_groups_host = g.n_groups_host;
   prm.kdim = g.kdim;

@@ -175,7 +175,12 @@ __global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_kernel(DispatchA
     }
     a.slot_dst[2 * j] = dev;
     a.slot_dst[2 * j + 1] = row;
-    if (dev >= 0) a.peer_g[dev][row] = a.w[j];
+    if (dev >= 0) {
+      a.peer_g[dev][row] = a.w[j];
+      // (source rank, flat slot) of this receive row: the GEMM2 epilogue pushes the row's output
+      // straight into slot j of this rank's slot buffer
+      if (a.peer_rsrc) a.peer_rsrc[dev][row] = (int32_t)((j << 5) | a.rank);
+    }
   }
   const int nv = a.D / 8;  // 16-byte vectors per row
   for (int src_i = 0; src_i < (a.x2 ? 2 : 1); ++src_i) {
@@ -399,6 +404,48 @@ __global__ void wait_flag_kernel(const uint32_t *flag, uint32_t v, int32_t *err)
   __threadfence_system();
 }
 
+// a10 with the pushed GEMM2 epilogue: every slot's gated output row already sits in this rank's
+// slot buffer [B*K, D]; out[t] = Σ_{k} slotbuf[t*K + k] in slot order (fp32, one bf16 rounding).
+template <int KM>
+__global__ void __launch_bounds__(kCombineWarps * 32) combine_local_kernel(const uint16_t *__restrict__ slotbuf,
+                                                                           int64_t B, int K, int D,
+                                                                           const int32_t *__restrict__ slot_dst,
+                                                                           uint16_t *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * kCombineWarps + (threadIdx.x >> 5);
+  if (t >= B) return;
+  const int nv = D / 8;
+  const int4 *src = reinterpret_cast<const int4 *>(slotbuf) + t * K * nv;
+  int valid = 0;  // slots whose expert id was in range (others contribute nothing)
+  if (lane < K) valid = slot_dst[2 * (t * K + lane)] >= 0;
+  const unsigned vm = __ballot_sync(0xffffffffu, valid);
+  int4 *dst = reinterpret_cast<int4 *>(out) + t * nv;
+  for (int i = lane; i < nv; i += 64) {
+    const bool two = i + 32 < nv;
+    int4 v0[KM], v1[KM];
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {
+      v0[k] = make_int4(0, 0, 0, 0);
+      v1[k] = make_int4(0, 0, 0, 0);
+      if (k < K && ((vm >> k) & 1)) {
+        v0[k] = __ldcs(src + k * nv + i);
+        if (two) v1[k] = __ldcs(src + k * nv + i + 32);
+      }
+    }
+    float acc0[8], acc1[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc0[u] = acc1[u] = 0.f;
+#pragma unroll
+    for (int k = 0; k < KM; ++k)
+      if (k < K) {
+        acc_bf16x8(acc0, v0[k]);
+        acc_bf16x8(acc1, v1[k]);
+      }
+    __stcs(dst + i, pack_bf16x8(acc0));
+    if (two) __stcs(dst + i + 32, pack_bf16x8(acc1));
+  }
+}
+
 // ----------------------------------------------------------------------- host read-back
 // Copies the plan blob, the layout summary and the error flags into mapped pinned host memory
 // with plain stores (zero-copy), so the one host synchronisation of the layer never queues
@@ -444,6 +491,18 @@ cudaError_t launch_signal(uint32_t *flag, uint32_t v, cudaStream_t s) {
 
 cudaError_t launch_wait_flag(const uint32_t *flag, uint32_t v, int32_t *err, cudaStream_t s) {
   wait_flag_kernel<<<1, 1, 0, s>>>(flag, v, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine_local(const uint16_t *slotbuf, int64_t B, int K, int D, const int32_t *slot_dst,
+                                 uint16_t *out, cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((B + kCombineWarps - 1) / kCombineWarps);
+  if (K <= 2) combine_local_kernel<2><<<blocks, kCombineWarps * 32, 0, s>>>(slotbuf, B, K, D, slot_dst, out);
+  else if (K <= 4) combine_local_kernel<4><<<blocks, kCombineWarps * 32, 0, s>>>(slotbuf, B, K, D, slot_dst, out);
+  else if (K <= 8) combine_local_kernel<8><<<blocks, kCombineWarps * 32, 0, s>>>(slotbuf, B, K, D, slot_dst, out);
+  else if (K <= 16) combine_local_kernel<16><<<blocks, kCombineWarps * 32, 0, s>>>(slotbuf, B, K, D, slot_dst, out);
+  else combine_local_kernel<32><<<blocks, kCombineWarps * 32, 0, s>>>(slotbuf, B, K, D, slot_dst, out);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,111 @@
+"""Critical-rank emulation of the 8-GPU comparison on one B200.
+
+For a scenario of the G120 layer (N=128, K=4, D=H=2880, 32K tokens per rank, P=8) the plans of all
+ranks are computed from the synthetic routing (host planner, bit-identical to the device one); for
+standard EP and for LLEP the most loaded rank's expert groups (rows per expert, in the layout
+kernel's order) are built and that rank's two grouped GEMMs are timed on this GPU through the C ABI
+(2-CTA kernels, CUDA events, median of several runs).  The GEMMs are ~93 % of a layer step at P=1;
+dispatch / combine / weight-broadcast costs over NVLink are NOT measured here.
+
+    python tools/emulate_p8.py [--scenarios 95:1,80:1,...] [--reps 5]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2601_17111_b200 import llep as L  # noqa: E402
+from synth import workload as W  # noqa: E402
+
+
+def rank_groups(plan, rank, M):
+    rows = []
+    for pass_ in (0, 1):
+        for e, chunks in enumerate(plan.chunks):
+            native = e // M == rank
+            if native != (pass_ == 0):
+                continue
+            r = sum(t - s for (d, s, t) in chunks if d == rank)
+            if r:
+                rows.append(r)
+    return rows
+
+
+class Gemms:
+    """The critical rank's grouped GEMM1 + GEMM2 on synthetic data (values do not matter for time)."""
+
+    def __init__(self, rows, D, H):
+        groups, rb = [], 0
+        for i, n in enumerate(rows):
+            groups.append((i, rb, n))
+            rb += (n + 255) // 256 * 256
+        E = len(rows)
+        self.groups, self.D, self.H = groups, D, H
+        self.x = torch.randn(rb, D, device="cuda").to(torch.bfloat16)
+        self.w13 = (torch.randn(E, 2 * H, D, device="cuda") / D ** 0.5).to(torch.bfloat16)
+        self.w2 = (torch.randn(E, D, H, device="cuda") / H ** 0.5).to(torch.bfloat16)
+        self.act = torch.empty(rb, H, device="cuda", dtype=torch.bfloat16)
+        self.y = torch.empty(rb, D, device="cuda", dtype=torch.bfloat16)
+        self.gate = torch.rand(rb, device="cuda")
+
+    def run_ms(self):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        L.grouped_gemm(0, self.x, self.w13, self.groups, self.H, out=self.act, pair=True)
+        L.grouped_gemm(1, self.act, self.w2, self.groups, self.D, gate=self.gate, out=self.y, pair=True)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="g120")
+    ap.add_argument("--world", type=int, default=8)
+    ap.add_argument("--scenarios", default="95:1,80:1,50:1,30:1,95:4,95:16,0:0")
+    ap.add_argument("--reps", type=int, default=5)
+    args = ap.parse_args()
+    base = W.CONFIGS[args.config]
+    P = args.world
+    sh = W.LayerShape(base.n_experts, base.top_k, base.d_model, base.d_ff, base.tokens_per_rank, P)
+    M = sh.experts_per_rank
+    out = []
+    for sc in args.scenarios.split(","):
+        pct, nhot = (int(v) for v in sc.split(":"))
+        hot = None if pct == 0 else pct
+        cnt = W.slot_counts(sh.n_experts, sh.tokens_per_rank * sh.top_k, hot, nhot)
+        loads = (cnt * P).tolist()   # every rank draws the same per-expert slot counts (exact multiset)
+        res = {"scenario": W.scenario_name(hot, nhot)}
+        g = {}
+        for mode in ("ep", "llep"):
+            plan = L.plan_host(loads, P, 1.0, 1024, 1.3, ep=(mode == "ep"))
+            per_rank = [sum(rank_groups(plan, r, M)) for r in range(P)]
+            crit = int(np.argmax(per_rank))
+            rows = rank_groups(plan, crit, M)
+            g[mode] = Gemms(rows, sh.d_model, sh.d_ff)
+            res[mode] = {"critical_rank": crit, "rows": int(sum(rows)), "groups": len(rows),
+                         "transfers": len(plan.transfers), "fallback": plan.fallback, "ms": []}
+        for m in ("ep", "llep"):
+            g[m].run_ms()                      # warm-up
+        for _ in range(args.reps):             # alternate so both see the same clock / power state
+            for m in ("ep", "llep"):
+                res[m]["ms"].append(g[m].run_ms())
+        for m in ("ep", "llep"):
+            res[m]["gemm_ms"] = statistics.median(res[m]["ms"])
+        del g
+        torch.cuda.empty_cache()
+        res["gemm_speedup"] = res["ep"]["gemm_ms"] / res["llep"]["gemm_ms"]
+        res["row_bound"] = res["ep"]["rows"] / res["llep"]["rows"]
+        print(json.dumps(res), flush=True)
+        out.append(res)
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -198,7 +198,10 @@ llep_status llep_prepare(llep_context *ctx, const int32_t *topk_ids, int64_t n_t
  *   x          [B, D] bf16, device      topk_ids [B, K] int32     topk_w [B, K] fp32
  *   w13        [M, 2H, D] bf16: rows 0..H-1 = W_gate,e, rows H..2H-1 = W_up,e (native experts)
  *   w2         [M, D, H] bf16 = W_down,e
- *   plan       device blob from llep_prepare of these topk_ids
+ *   plan       device blob from llep_prepare of these topk_ids.  The context caches the host copy
+ *              and the layout of the last plan by ADDRESS: a plan at another address is laid out
+ *              and validated again (chunk totals == loads, else LLEP_ERR_PLAN); do not overwrite
+ *              a prepared plan in place between llep_prepare and llep_moe_forward/backward
  *   out        [B, D] bf16, device
  * Errors: INVALID, PLAN (plan larger than the arena), CUDA, COMM. */
 llep_status llep_moe_forward(llep_context *ctx, const uint16_t *x, const int32_t *topk_ids,

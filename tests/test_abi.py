@@ -94,3 +94,38 @@ def test_host_plan_golden_and_paper_configs(L, golden_dir):
                     continue
                 l = (cnt * P).tolist()
                 _same(L.plan_host(l, P), O1.plan(l, P))
+
+
+def test_context_create_validation(L):
+    """Shape rules of llep_context_create are checked before any CUDA call: CPU-testable."""
+    import ctypes
+    bad = [
+        (6, 2, 256, 512, 4),     # N % P != 0
+        (8, 9, 256, 512, 2),     # K > N
+        (8, 0, 256, 512, 2),     # K < 1
+        (8, 2, 250, 512, 2),     # D % 8 != 0
+        (8, 2, 256, 4, 2),       # H < 8
+        (64, 2, 256, 512, 64),   # P > 32
+        (2048, 2, 256, 512, 2),  # N > 1024
+    ]
+    for (N, K, D, H, P) in bad:
+        sh = L.Shape(N, K, D, H, P)
+        h = ctypes.c_void_p()
+        code = L._lib.llep_context_create(ctypes.byref(sh), 0, 0, 16, ctypes.byref(h))
+        assert code == 1, (N, K, D, H, P, code)
+        assert L._lib.llep_last_error()
+    sh = L.Shape(8, 2, 256, 512, 2)
+    h = ctypes.c_void_p()
+    assert L._lib.llep_context_create(ctypes.byref(sh), 2, 0, 16, ctypes.byref(h)) == 1   # rank >= P
+
+
+def test_plan_bytes_formula(L):
+    """Blob layout: header, g_a [P] int64, n_chunks [N] int32, chunks [N][P+1] x 12 B, replica [N][P]."""
+    for N, P in [(8, 2), (128, 8), (384, 32), (1, 1)]:
+        a8 = lambda x: (x + 7) // 8 * 8
+        off = a8(64)
+        off = a8(off + 8 * P)
+        off = a8(off + 4 * N)
+        off = a8(off + 12 * N * (P + 1))
+        off = a8(off + N * P)
+        assert L.plan_bytes(N, P) == off

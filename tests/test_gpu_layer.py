@@ -215,3 +215,40 @@ def test_g120_p8_processes_one_gpu(L, tmp_path, pct, nhot):
         mr, l2 = LC.errors(res[p]["llep"].astype(np.float64), ref)
         assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (p, mr, l2)
         assert bool(res[p]["same"])
+
+
+def test_memory_cap_nomem(L):
+    """A plan whose receive rows exceed the context's memory cap fails with LLEP_ERR_NOMEM (the Q3
+    'tight memory cap' configuration), and the context stays usable under a larger cap."""
+    sh = W.LayerShape(8, 2, 256, 512, 1024, 1)
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, 95, 1, 5, "cuda")
+    ctx = L.Context(8, 2, 256, 512, 1, 0, 0, 1024)
+    ctx.enable_backward()
+    ctx.set_memory_cap(ctx.device_bytes() + 1024)   # nothing can grow
+    dout = torch.zeros_like(x)
+    with pytest.raises(L.LLEPError) as ei:
+        plan, _ = ctx.prepare(ids)
+        ctx.reserve(1 << 20, 4, 4)
+    assert ei.value.code == 4
+    ctx.set_memory_cap(0)
+    out = ctx(x, ids, gates, w13, w2)
+    torch.cuda.synchronize()
+    ref = LC.oracle_rank_output(sh, 0, ids_np, g_np, 5)
+    mr, l2 = LC.errors(out.float().cpu().numpy().astype(np.float64), ref)
+    assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2
+    ctx.close()
+
+
+def test_inconsistent_plan_rejected(L):
+    """A plan whose chunk totals differ from the exchanged loads -> LLEP_ERR_PLAN."""
+    sh = W.LayerShape(8, 2, 256, 512, 1024, 1)
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, 95, 1, 5, "cuda")
+    ctx = L.Context(8, 2, 256, 512, 1, 0, 0, 1024)
+    good, _ = ctx.prepare(ids)          # kept alive: plans are identified by address
+    other = L.plan_host([100] * 8, 1, 1.0, 0, 1.0)
+    bad = torch.frombuffer(bytearray(other.raw), dtype=torch.uint8).cuda()
+    with pytest.raises(L.LLEPError) as ei:
+        ctx.forward(x, ids, gates, w13, w2, bad)
+    assert ei.value.code == 2
+    ctx.forward(x, ids, gates, w13, w2, good)   # the prepared plan still works
+    ctx.close()

@@ -94,7 +94,19 @@ __global__ void __launch_bounds__(kPlanThreads) planner_kernel(
   // λ test: balanced iff max(l)/mean(l) < λ; S == 0 counts as balanced (R9)
   bool fallback = (S == 0) ||
                   (__ddiv_rn((double)maxl, __ddiv_rn((double)S, (double)N)) < lambda);
-  const bool native_only = force_ep || fallback;
+  // If cap >= every device's native load, every expert is Case 1 of Alg. 2: LLA's plan
+  // is the all-native one (exactly; the sequential loop is skipped).  Not a λ fallback.
+  bool all_case1 = false;
+  if (!force_ep && !fallback) {
+    long long gmax = 0;
+    for (int d = 0; d < P; ++d) {
+      long long gn = 0;
+      for (int e = d * M; e < (d + 1) * M; ++e) gn += sm_l[e];
+      gmax = gn > gmax ? gn : gmax;
+    }
+    all_case1 = cap >= gmax;
+  }
+  const bool native_only = force_ep || fallback || all_case1;
 
   if (native_only) {
     // standard EP (Alg. 1) / λ fallback: every expert's load on its native device
@@ -325,22 +337,35 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(LayoutArgs a) {
     }
   }
   __syncthreads();
-  // m-block schedule of this rank's grouped GEMMs: small groups interleaved among big ones
-  if (tid == 0) {
-    int nb = 0, ns = 0;
+  // m-block schedule of this rank's grouped GEMMs: small groups interleaved among big ones.
+  // Warp 0 scans the groups' block counts per class (big / small) 32 groups at a time.
+  if (warp == 0) {
     const int G = sm_groups < kMaxGroups ? sm_groups : kMaxGroups;
-    for (int g = 0; g < G; ++g) {
-      const int mb = (a.groups[g].n_rows + a.row_align - 1) / a.row_align;
-      if (mb * a.row_align > kSmallGroupRows) {
-        sm_before[g] = nb;
-        nb += mb;
-      } else {
-        sm_before[g] = ns;
-        ns += mb;
+    int nb = 0, ns = 0;
+    for (int base = 0; base < G; base += 32) {
+      const int g = base + lane;
+      int mb = 0;
+      bool big = false;
+      if (g < G) {
+        mb = (a.groups[g].n_rows + a.row_align - 1) / a.row_align;
+        big = mb * a.row_align > kSmallGroupRows;
       }
+      int ib = big ? mb : 0, is = big ? 0 : mb;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ub = __shfl_up_sync(0xffffffffu, ib, o), us = __shfl_up_sync(0xffffffffu, is, o);
+        if (lane >= o) {
+          ib += ub;
+          is += us;
+        }
+      }
+      if (g < G) sm_before[g] = big ? nb + ib - mb : ns + is - mb;
+      nb += __shfl_sync(0xffffffffu, ib, 31);
+      ns += __shfl_sync(0xffffffffu, is, 31);
     }
-    sm_nbig = nb;
-    sm_nsmall = ns;
+    if (lane == 0) {
+      sm_nbig = nb;
+      sm_nsmall = ns;
+    }
   }
   __syncthreads();
   if (sm_mblocks <= a.sched_cap && sm_groups <= kMaxGroups) {

@@ -39,18 +39,35 @@ __global__ void __launch_bounds__(kCountThreads) tile_count_kernel(
     tile_cnt[(size_t)blockIdx.x * N + e] = hist[e];
 }
 
-// exclusive scan over tiles per expert -> tile offsets; totals = this rank's counts row
-__global__ void tile_scan_kernel(const int32_t *__restrict__ tile_cnt, int n_tiles, int N,
-                                 int32_t *__restrict__ tile_off, int32_t *__restrict__ cnt) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= N) return;
+// exclusive scan over tiles per expert -> tile offsets; totals = this rank's counts row.
+// One block per 32 experts (lane = expert, coalesced), 8 warps each own a contiguous eighth of the
+// tiles: pass 1 sums each warp's share, the warp bases are scanned in shared memory, pass 2 writes.
+constexpr int kScanWarps = 8;
+
+__global__ void __launch_bounds__(kScanWarps * 32) tile_scan_kernel(const int32_t *__restrict__ tile_cnt,
+                                                                    int n_tiles, int N,
+                                                                    int32_t *__restrict__ tile_off,
+                                                                    int32_t *__restrict__ cnt) {
+  __shared__ int part[kScanWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  const int per = (n_tiles + kScanWarps - 1) / kScanWarps;
+  const int t0 = warp * per, t1 = min(n_tiles, t0 + per);
+  int s = 0;
+  if (e < N)
+    for (int t = t0; t < t1; ++t) s += tile_cnt[(size_t)t * N + e];
+  part[warp][lane] = s;
+  __syncthreads();
   int run = 0;
-  for (int t = 0; t < n_tiles; ++t) {
-    const int v = tile_cnt[(size_t)t * N + e];
-    tile_off[(size_t)t * N + e] = run;
-    run += v;
+  for (int w = 0; w < warp; ++w) run += part[w][lane];
+  if (e < N) {
+    for (int t = t0; t < t1; ++t) {
+      const int v = tile_cnt[(size_t)t * N + e];
+      tile_off[(size_t)t * N + e] = run;
+      run += v;
+    }
+    if (warp == kScanWarps - 1) cnt[e] = run;
   }
-  cnt[e] = run;
 }
 
 // ----------------------------------------------------------------- a3: stable local ranks r_j
@@ -526,7 +543,7 @@ cudaError_t launch_tile_count(const int32_t *ids, int64_t n_slots, int32_t N, in
 
 cudaError_t launch_tile_scan(const int32_t *tile_cnt, int32_t n_tiles, int32_t N, int32_t *tile_off,
                              int32_t *cnt, cudaStream_t s) {
-  tile_scan_kernel<<<(N + 127) / 128, 128, 0, s>>>(tile_cnt, n_tiles, N, tile_off, cnt);
+  tile_scan_kernel<<<(N + 31) / 32, kScanWarps * 32, 0, s>>>(tile_cnt, n_tiles, N, tile_off, cnt);
   return cudaGetLastError();
 }
 

@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -402,10 +403,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
 // CTAs' TMA loads complete on the leader's full barrier; the MMA commits are multicast to both
 // CTAs' empty / accumulator-full barriers; each CTA's epilogue drains its own TMEM lanes (its 128
 // rows of the 256-row accumulator) and arrives on the leader's TMEM-empty barrier.
-template <int BN>
+template <int BN, int KSUB = 1>   // KSUB: 64-deep K sub-tiles per pipeline stage
 struct Cfg2 {
-  static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int A_BYTES = BM * BK * 2 * KSUB;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2 * KSUB;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int EXTRA = 1024 + 256;
   static constexpr int STAGES_RAW = (kSmemBudget - EXTRA) / STAGE;
@@ -464,9 +465,10 @@ __device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
       : "memory");
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, int KSUB>
 __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(const __grid_constant__ GemmParams p) {
-  using C = Cfg2<BN>;
+  using C = Cfg2<BN, KSUB>;
+  constexpr int KST = BK * KSUB;                 // K per pipeline stage
   constexpr int S = C::STAGES;
   constexpr int TM = 2 * BM;                     // rows per pair tile
   constexpr int BH = BN / 2;                     // B rows staged by each CTA
@@ -515,7 +517,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
     const Group last = p.groups[n_groups - 1];
     total_tiles = (last.mblk_start + (last.n_rows + TM - 1) / TM) * p.n_ntiles;
   }
-  const int nk = (p.kdim + BK - 1) / BK;
+  const int nk = (p.kdim + KST - 1) / KST;
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
 
   if (warp == 0) {
@@ -535,13 +537,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
         wait_weights(p, ti.wslot);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
+          const int nsub = min(KSUB, (p.kdim - kb * KST + BK - 1) / BK);   // skip all-OOB sub-tiles
           const uint32_t fl = smem_u32(full + stage);
-          if (leader) mbar_expect_tx(fl, 2 * C::STAGE);
+          if (leader) mbar_expect_tx(fl, 2 * nsub * (C::STAGE / KSUB));
           const uint32_t fb = mapa_shared(fl, 0);
-          tma_load_2d_pair(smem_u32(sA + stage * C::A_BYTES), &p.tmA, fb, kb * BK,
-                           ti.row0 + (int)crank * BM, pol_act);
-          tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES), wm, fb, kb * BK, brow,
-                           ti.small ? pol_first : pol_last);
+          for (int s2 = 0; s2 < nsub; ++s2) {
+            tma_load_2d_pair(smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128)), &p.tmA, fb,
+                             (kb * KSUB + s2) * BK, ti.row0 + (int)crank * BM, pol_act);
+            tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES + s2 * ((BN / 2) * 128)), wm, fb,
+                             (kb * KSUB + s2) * BK, brow, ti.small ? pol_first : pol_last);
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -568,10 +573,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+          const int nsub = min(KSUB, (p.kdim - kb * KST + BK - 1) / BK);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            tc_mma_pair(d_tmem, smem_desc(a0 + kk * 32), smem_desc(b0 + kk * 32), idesc,
-                        (kb | kk) != 0);
+          for (int s2 = 0; s2 < KSUB; ++s2) {
+            if (s2 < nsub) {
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk)
+                tc_mma_pair(d_tmem, smem_desc(a0 + s2 * (BM * 128) + kk * 32),
+                            smem_desc(b0 + s2 * ((BN / 2) * 128) + kk * 32), idesc, (kb | s2 | kk) != 0);
+            }
+          }
           tc_commit_pair(smem_u32(empty + stage));
           if (++stage == S) {
             stage = 0;
@@ -728,10 +739,10 @@ llep_status launch(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
   return LLEP_OK;
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, int KSUB = 2>
 llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
-  using C = Cfg2<BN>;
-  auto kern = grouped_gemm_2cta_kernel<BN, MODE>;
+  using C = Cfg2<BN, KSUB>;
+  auto kern = grouped_gemm_2cta_kernel<BN, MODE, KSUB>;
   static bool attr_set = false;
   if (!attr_set) {
     LLEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1539,6 +1550,21 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   prm.gate = g.gate;
   prm.out = reinterpret_cast<__nv_bfloat16 *>(g.out);
   if (g.row_align == 2 * BM) {   // 2-CTA pair tiles (groups 256-row aligned)
+    if (getenv("LLEP_FWD_KSUB1")) {                   // A/B: 64-deep pipeline stages
+      if (g.mode == 0) return g.nout % 120 == 0 && g.nout % 128 ? launch_pair<240, 0, 1>(g, prm, s)
+                                                             : launch_pair<256, 0, 1>(g, prm, s);
+      if (g.mode == 1) return g.nout % 240 == 0 && g.nout % 256 ? launch_pair<240, 1, 1>(g, prm, s)
+                                                             : launch_pair<256, 1, 1>(g, prm, s);
+    }
+    if (const char *fb = getenv("LLEP_FWD_BN")) {   // A/B override of the tile width
+      const int bn = atoi(fb);
+      if (g.mode == 0 && bn == 192) return launch_pair<192, 0>(g, prm, s);
+      if (g.mode == 0 && bn == 256) return launch_pair<256, 0>(g, prm, s);
+      if (g.mode == 0 && bn == 240) return launch_pair<240, 0>(g, prm, s);
+      if (g.mode == 1 && bn == 192) return launch_pair<192, 1>(g, prm, s);
+      if (g.mode == 1 && bn == 256) return launch_pair<256, 1>(g, prm, s);
+      if (g.mode == 1 && bn == 240) return launch_pair<240, 1>(g, prm, s);
+    }
     if (g.mode == 0) {
       if (g.nout % 128 == 0) return launch_pair<256, 0>(g, prm, s);
       if (g.nout % 120 == 0) return launch_pair<240, 0>(g, prm, s);

@@ -458,6 +458,26 @@ __device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t adesc, uin
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-converged issue: the whole MMA warp runs the loop (so descriptors live in uniform
+// registers) and one elected lane issues.
+__device__ __forceinline__ void tc_mma_pair_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair_w(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+      ::"r"(bar), "h"((uint16_t)3)
+      : "memory");
+}
 __device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
@@ -471,7 +491,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
   constexpr int KST = BK * KSUB;                 // K per pipeline stage
   constexpr int S = C::STAGES;
   constexpr int TM = 2 * BM;                     // rows per pair tile
-  constexpr int BH = BN / 2;                     // B rows staged by each CTA
   constexpr int BNO = MODE != 1 ? BN / 2 : BN;   // output columns per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -533,7 +552,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
         const TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
         const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
         const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
-        const int brow = MODE != 1 ? wbase + (int)crank * p.wup_off : wbase + (int)crank * BH;
+        const int brow = MODE != 1 ? wbase + (int)crank * p.wup_off : wbase + (int)crank * (BN / 2);
         wait_weights(p, ti.wslot);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
@@ -555,10 +574,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      // ---------------------------------------------------------------- MMA issuer (leader)
+    if (leader) {
+      // ---------------------------------------------------------------- MMA issuer (leader warp)
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(TM >> 4) << 24);
+      const uint64_t adesc0 = smem_desc(smem_u32(sA)), bdesc0 = smem_desc(smem_u32(sB));
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -571,25 +591,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(full + stage), phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+          __syncwarp();
+          // descriptor start-address field is addr >> 4: advance it by the byte offset >> 4
+          const uint64_t ad = adesc0 + (uint32_t)((stage * C::A_BYTES) >> 4);
+          const uint64_t bd = bdesc0 + (uint32_t)((stage * C::B_BYTES) >> 4);
           const int nsub = min(KSUB, (p.kdim - kb * KST + BK - 1) / BK);
 #pragma unroll
           for (int s2 = 0; s2 < KSUB; ++s2) {
             if (s2 < nsub) {
 #pragma unroll
               for (int kk = 0; kk < BK / 16; ++kk)
-                tc_mma_pair(d_tmem, smem_desc(a0 + s2 * (BM * 128) + kk * 32),
-                            smem_desc(b0 + s2 * ((BN / 2) * 128) + kk * 32), idesc, (kb | s2 | kk) != 0);
+                tc_mma_pair_w(d_tmem, ad + (uint32_t)((s2 * (BM * 128) + kk * 32) >> 4),
+                              bd + (uint32_t)((s2 * ((BN / 2) * 128) + kk * 32) >> 4), idesc,
+                              (kb | s2 | kk) != 0);
             }
           }
-          tc_commit_pair(smem_u32(empty + stage));
+          tc_commit_pair_w(smem_u32(empty + stage));
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit_pair(smem_u32(tfull + acc));
+        tc_commit_pair_w(smem_u32(tfull + acc));
       }
     }
   } else {
@@ -606,14 +629,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       const bool row_ok = row < ti.row_end;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
       const int col0 = ti.nb * BNO;
+      constexpr int bno = BNO;
       if (MODE == 2) {
         // raw gate / up pre-activations for the backward recompute: GU[r] = [g (nout) | u (nout)]
         __nv_bfloat16 *grow = p.out + (size_t)row * 2 * p.nout + col0;
 #pragma unroll 1
-        for (int j = 0; j < BNO; j += 8) {
+        for (int j = 0; j < bno; j += 8) {
           float g[8], u[8];
           tmem_ld8(taddr + j, g);
-          tmem_ld8(taddr + BNO + j, u);
+          tmem_ld8(taddr + bno + j, u);
           tmem_ld_wait();
           if (row_ok && col0 + j < p.nout) {
             uint4 og, ou;
@@ -631,10 +655,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       } else if (MODE == 0) {
         __nv_bfloat16 *orow = p.out + (size_t)row * p.nout + col0;
 #pragma unroll 1
-        for (int j = 0; j < BNO; j += 8) {
+        for (int j = 0; j < bno; j += 8) {
           float g[8], u[8];
           tmem_ld8(taddr + j, g);
-          tmem_ld8(taddr + BNO + j, u);
+          tmem_ld8(taddr + bno + j, u);
           tmem_ld_wait();
           if (row_ok && col0 + j < p.nout) {
             uint4 o;
@@ -656,7 +680,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
           orow = reinterpret_cast<__nv_bfloat16 *>(p.peer_slot[src & 31]) + (size_t)(src >> 5) * p.nout + col0;
         }
 #pragma unroll 1
-        for (int j = 0; j < BNO; j += 8) {
+        for (int j = 0; j < bno; j += 8) {
           float v[8];
           tmem_ld8(taddr + j, v);
           tmem_ld_wait();

@@ -75,6 +75,9 @@ def _ref_gemm(mode, a, w, groups, nout, gate):
     (1, 768, 2048),   # Qwen3 GEMM2
     (0, 192, 200),    # ragged: masked tail tile, partial K block
     (1, 200, 136),
+    (0, 128, 144),    # masked tail tiles at other widths
+    (1, 256, 288),
+    (0, 136, 264),
 ])
 def test_grouped_gemm(L, mode, kdim, nout, pair):
     g = torch.Generator(device="cuda").manual_seed(kdim * 7 + nout)

@@ -12,6 +12,8 @@ never imports it.
                      per-slot destinations from the plan
     O3  layer.py     Eq. 1 with SwiGLU experts, float64
     O4  simulate.py  Alg. 1 / Alg. 4 executed per simulated device
+    O5  backward.py  gradients of Eq. 1 + spilled-expert weight-gradient return
+    O6  router.py    the router of Eq. 2: softmax over N, top-K, gates = s
 
 Pins (tests/test_oracle_*.py, `-m "not gpu"`): SPEC hand traces (tests/golden/),
 the §2.1 worked example, closed-form load accounting, invariants,

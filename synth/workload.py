@@ -26,7 +26,7 @@ M32 = 0xFFFFFFFF
 _MUL = 0x45D9F3B  # < 2^31: (x ^ x>>16) * _MUL stays below 2^63 in int64
 
 # tensor tags for the counter streams
-TAG_X, TAG_WGATE, TAG_WUP, TAG_WDOWN, TAG_GATE = 1, 2, 3, 4, 5
+TAG_X, TAG_WGATE, TAG_WUP, TAG_WDOWN, TAG_GATE, TAG_WROUTER = 1, 2, 3, 4, 5, 6
 
 
 @dataclass(frozen=True)
@@ -174,6 +174,20 @@ def expert_weights_torch(experts, D: int, H: int, device, seed: int = BASE_SEED)
         w13[i, H:] = _uniform_f32_torch(stream_key(seed, TAG_WUP, e), H * D, w_in_amp(D), device).to(torch.bfloat16).reshape(H, D)
         w2[i] = _uniform_f32_torch(stream_key(seed, TAG_WDOWN, e), D * H, w_out_amp(H), device).to(torch.bfloat16).reshape(D, H)
     return w13, w2
+
+
+def router_weight_bits(N: int, D: int, scale: float = 1.0, seed: int = BASE_SEED) -> np.ndarray:
+    """Router weight stored as [N, D] bf16 bits (row i = column i of the paper's W_r ∈ R^{D×N}),
+    uniform with variance scale²/D, so unit-variance tokens give logits of standard deviation ~scale."""
+    f = _uniform_f32_np(stream_key(seed, TAG_WROUTER, N), N * D, scale * w_in_amp(D))
+    return bf16_bits_from_f32(f).reshape(N, D)
+
+
+def router_weight_torch(N: int, D: int, device, scale: float = 1.0, seed: int = BASE_SEED):
+    """Same values as router_weight_bits, as a bf16 tensor on `device`."""
+    import torch
+    f = _uniform_f32_torch(stream_key(seed, TAG_WROUTER, N), N * D, scale * w_in_amp(D), device)
+    return f.to(torch.bfloat16).reshape(N, D)
 
 
 # --------------------------------------------------------------------------- routing

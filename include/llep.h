@@ -299,6 +299,24 @@ llep_status llep_gemm_bwd(int32_t kind, const uint16_t *a, const uint16_t *w_or_
                           int32_t kdim_or_mdim, int32_t nout, int32_t n_weights, const int32_t *groups,
                           int32_t n_groups, void *out, void *stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * Router (row f4): Eq. 2 of PAPER.md for one rank's tokens, producing the top-K ids and
+ * gates that llep_prepare / llep_moe_forward consume.
+ *   z[t, i]  = Σ_d x[t, d] · w_router[i, d]        (w_router [N, D] = W_rᵀ, one row per expert)
+ *   s[t, :]  = softmax(z[t, :]) over all N experts (fp32, max-subtracted, Σ in expert order)
+ *   topk_ids[t, k]  = the k-th largest s[t, :], descending, ties -> lower expert id (DESIGN R31/R32)
+ *   topk_w[t, k]    = s[t, topk_ids[t, k]]          (no renormalisation over the K: Eq. 2 writes none)
+ * x: DEVICE bf16 [n_tokens, d_model] row-major; w_router: DEVICE bf16 [n_experts, d_model];
+ * topk_ids: DEVICE int32 [n_tokens, top_k]; topk_w: DEVICE fp32 [n_tokens, top_k];
+ * logits: DEVICE fp32 [n_tokens, n_experts] or NULL (a copy of z, for tests).  Caller-owned; the
+ * library keeps no pointer.  z accumulates in fp32 on the tensor cores (bf16 products are exact).
+ * Limits: 1 <= n_experts <= 512, 1 <= top_k <= min(16, n_experts), d_model % 8 == 0, 16-byte
+ * aligned x / w_router.  n_tokens == 0 is a no-op.  Stream-ordered on `stream`.
+ * Errors: INVALID (limits, null pointers, alignment), CUDA. */
+llep_status llep_router(const uint16_t *x, const uint16_t *w_router, int64_t n_tokens, int32_t d_model,
+                        int32_t n_experts, int32_t top_k, int32_t *topk_ids, float *topk_w,
+                        float *logits, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1205,6 +1205,27 @@ llep_status llep_debug_copy(llep_context *c, int32_t what, void *dst, int64_t n,
   return LLEP_OK;
 }
 
+llep_status llep_router(const uint16_t *x, const uint16_t *w_router, int64_t n_tokens, int32_t d_model,
+                        int32_t n_experts, int32_t top_k, int32_t *topk_ids, float *topk_w,
+                        float *logits, void *stream) {
+  if (n_tokens < 0) return invalid("n_tokens < 0");
+  if (n_experts < 1 || n_experts > 512) return invalid("router: n_experts must be in [1, 512]");
+  if (top_k < 1 || top_k > 16 || top_k > n_experts) return invalid("router: top_k must be in [1, min(16, N)]");
+  if (d_model < 8 || d_model % 8) return invalid("router: d_model must be a positive multiple of 8");
+  if (n_tokens == 0) return LLEP_OK;
+  if (!x || !w_router || !topk_ids || !topk_w) return invalid("null pointer");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w_router)) & 15)
+    return invalid("router: x and w_router must be 16-byte aligned");
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    LLEP_CUDA(cudaGetDevice(&dev));
+    LLEP_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  RouterArgs a{x, w_router, n_tokens, d_model, n_experts, top_k, topk_ids, topk_w, logits, num_sms};
+  return run_router(a, (cudaStream_t)stream);
+}
+
 llep_status llep_grouped_gemm(int32_t mode, const uint16_t *a, int64_t rows, int32_t kdim,
                               const uint16_t *w, int32_t n_weights, int32_t nout,
                               const int32_t *groups, int32_t n_groups, const float *gate,

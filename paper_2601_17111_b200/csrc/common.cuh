@@ -233,6 +233,17 @@ struct BwdArgs {
   int32_t pair;               // 1: 2-CTA (cta_group::2) variant, 256-row / 256-output-row pair tiles
 };
 llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s);
+
+// router of Eq. 2 (row f4, router.cu)
+struct RouterArgs {
+  const void *x, *w_router;
+  int64_t n_tokens;
+  int32_t d_model, n_experts, top_k;
+  int32_t *ids;
+  float *gates, *logits;
+  int32_t num_sms;
+};
+llep_status run_router(const RouterArgs &a, cudaStream_t s);
 // host: workspace floats of a kind-1 launch over groups with these row counts; reduce the partials
 int64_t wgrad_workspace(const int32_t *n_rows, int n_groups, int mdim, int nout, int num_sms);
 llep_status reduce_wgrad_splits(const BwdArgs &a, const int32_t *n_rows, const int32_t *wslots,

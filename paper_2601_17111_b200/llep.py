@@ -80,6 +80,7 @@ _SIGS = {
     "llep_context_stats": (ctypes.c_int, [_vp, ctypes.c_void_p, _i32]),
     "llep_gemm_bwd": (ctypes.c_int, [_i32, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
     "llep_grouped_gemm": (ctypes.c_int, [_i32, _vp, _i64, _i32, _vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
+    "llep_router": (ctypes.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
 }
 EXPORTS = tuple(_SIGS)
 for _name, (_res, _args) in _SIGS.items():
@@ -302,6 +303,24 @@ class Context:
         t = torch.empty(n, dtype=dtype, device=f"cuda:{self.device}")
         _check(_lib.llep_debug_copy(self._h, what, t.data_ptr(), n, _stream_ptr()))
         return t
+
+
+def router(x, w_router, top_k: int, logits: bool = False, out=None):
+    """llep_router (row f4, Eq. 2): x [B, D] bf16, w_router [N, D] bf16 (= W_rᵀ) on the current
+    device -> (topk_ids int32 [B, K], topk_w fp32 [B, K]) [+ logits fp32 [B, N] if logits=True].
+    `out` = (ids, gates) preallocated tensors, optional."""
+    import torch
+    B, D = x.shape
+    N = w_router.shape[0]
+    if out is None:
+        ids = torch.empty((B, top_k), dtype=torch.int32, device=x.device)
+        gates = torch.empty((B, top_k), dtype=torch.float32, device=x.device)
+    else:
+        ids, gates = out
+    z = torch.empty((B, N), dtype=torch.float32, device=x.device) if logits else None
+    _check(_lib.llep_router(x.data_ptr(), w_router.data_ptr(), B, D, N, top_k, ids.data_ptr(), gates.data_ptr(),
+                            z.data_ptr() if z is not None else None, _stream_ptr()))
+    return (ids, gates, z) if logits else (ids, gates)
 
 
 def grouped_gemm(mode: int, a, w, groups: Sequence[Tuple[int, int, int]], nout: int, gate=None, out=None,

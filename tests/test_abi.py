@@ -1,5 +1,6 @@
 """The C-ABI library loads, exports every symbol llep.h declares, and its HOST planner
 (llep_plan / llep_plan_ep, no GPU needed) is bit-identical to the oracle -- CPU only."""
+import ctypes
 import os
 import random
 import re
@@ -129,3 +130,27 @@ def test_plan_bytes_formula(L):
         off = a8(off + 12 * N * (P + 1))
         off = a8(off + N * P)
         assert L.plan_bytes(N, P) == off
+
+
+def test_router_validation(L):
+    """llep_router rejects out-of-range arguments with LLEP_ERR_INVALID before touching the device;
+    an empty batch is a no-op that returns OK (no CUDA call)."""
+    lib = L._lib
+    buf = (ctypes.c_uint16 * 64)()
+    ids = (ctypes.c_int32 * 8)()
+    g = (ctypes.c_float * 8)()
+    p = ctypes.addressof(buf)
+    cases = [
+        (p, p, 4, 64, 0, 1),      # N < 1
+        (p, p, 4, 64, 513, 2),    # N > 512
+        (p, p, 4, 64, 8, 0),      # K < 1
+        (p, p, 4, 64, 8, 9),      # K > N
+        (p, p, 4, 64, 32, 17),    # K > 16
+        (p, p, 4, 60, 8, 2),      # D % 8
+        (p, p, -1, 64, 8, 2),     # negative batch
+        (None, p, 4, 64, 8, 2),   # null x
+    ]
+    for (x, w, B, D, N, K) in cases:
+        assert lib.llep_router(x, w, B, D, N, K, ctypes.addressof(ids), ctypes.addressof(g), None, None) == 1
+        assert lib.llep_last_error()
+    assert lib.llep_router(None, None, 0, 64, 8, 2, None, None, None, None) == 0

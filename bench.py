@@ -213,6 +213,37 @@ def run_backward(L, ctx, shape, inputs, steps, warmup, world, seed):
     return max_over_ranks(e0.elapsed_time(e1), world) / steps
 
 
+def run_router(L, shape, x, steps, warmup):
+    """Row f4: llep_router (Eq. 2) on this rank's tokens, CUDA-event timed.  Not inside the layer
+    step (the north-star metric takes the routing as input); reported beside it."""
+    import torch
+    N, K, D = shape.n_experts, shape.top_k, shape.d_model
+    w_r = W.router_weight_torch(N, D, x.device)
+    out = (torch.empty((x.shape[0], K), dtype=torch.int32, device=x.device),
+           torch.empty((x.shape[0], K), dtype=torch.float32, device=x.device))
+    for _ in range(warmup):
+        L.router(x, w_r, K, out=out)
+    torch.cuda.synchronize()
+    # one call captured in a CUDA graph and replayed: device time, not the Python launch rate
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        L.router(x, w_r, K, out=out)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    B = x.shape[0]
+    nbytes = B * D * 2 + N * D * 2 + B * K * 8
+    return {"ms_per_call": ms, "bytes_per_call": nbytes, "gbs": nbytes / (ms / 1e3) / 1e9,
+            "tflops": 2.0 * B * N * D / (ms / 1e3) / 1e12,
+            "note": "x [B,D] bf16 read once (189 MB at G120, > L2) + W_r + ids/gates written"}
+
+
 def run_e2e(L, ctx, shape, host, dev, steps, warmup, world, ep=False):
     """Public API end to end: every step copies its inputs from pinned host memory (H2D), runs the
     layer (llep_prepare + llep_moe_forward) and reads the output back (D2H).  Double-buffered: the
@@ -364,6 +395,7 @@ def gpu_main(args):
     if not args.no_backward:
         bwd_ms = run_backward(L, ll_ctx, shape, inputs, max(3, args.steps // 2), 3, world, SEED)
     ll_ctx.close()
+    router = run_router(L, shape, x, max(10, args.steps), 3)
 
     sweep = []
     if args.sweep:
@@ -446,6 +478,8 @@ def gpu_main(args):
                             "tflops": bwd_flops / (bwd_ms / 1e3) / 1e12,
                             "note": "llep_prepare + llep_moe_backward (recomputes the forward internals; "
                                     "dx, dgates, dW13, dW_down incl. spilled-expert gradient return)"}
+    router["frac_hbm"] = router["gbs"] / peaks["hbm_gbs"]
+    line["router"] = router
     if e2e:
         line["e2e"] = e2e
     if sweep:

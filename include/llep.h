@@ -303,7 +303,8 @@ llep_status llep_gemm_bwd(int32_t kind, const uint16_t *a, const uint16_t *w_or_
  * Router (row f4): Eq. 2 of PAPER.md for one rank's tokens, producing the top-K ids and
  * gates that llep_prepare / llep_moe_forward consume.
  *   z[t, i]  = Σ_d x[t, d] · w_router[i, d]        (w_router [N, D] = W_rᵀ, one row per expert)
- *   s[t, :]  = softmax(z[t, :]) over all N experts (fp32, max-subtracted, Σ in expert order)
+ *   s[t, :]  = softmax(z[t, :]) over all N experts (fp32, max-subtracted; Σ accumulated online in
+ *              expert order, rescaled to the running max once per 64 experts)
  *   topk_ids[t, k]  = the k-th largest s[t, :], descending, ties -> lower expert id (DESIGN R31/R32)
  *   topk_w[t, k]    = s[t, topk_ids[t, k]]          (no renormalisation over the K: Eq. 2 writes none)
  * x: DEVICE bf16 [n_tokens, d_model] row-major; w_router: DEVICE bf16 [n_experts, d_model];

@@ -7,8 +7,9 @@
 //   warp 0      TMA producer: token tile [128 x 64] (evict-first: streamed once) + the router weight
 //               [Npad x 64] (evict-last: every tile re-reads it from L2), 128-byte swizzle
 //   warp 1      TMEM allocator + warp-converged tcgen05.mma issue (M=128, N=box, K=16 steps)
-//   warps 2-5   epilogue, one token row per thread: tcgen05.ld of the fp32 logits, running max and
-//               a register top-K insertion (pass 1), Σ exp(z - max) (pass 2), gates = exp / Σ.
+//   warps 2-5   epilogue, one token row per thread, one pass over the fp32 logits in TMEM (64
+//               columns per wait): online softmax (running max, Σ exp rescaled per chunk) and a
+//               branch-free register top-K insertion; gates = exp(z - max) / Σ.
 // The logits never touch HBM (optional debug copy).  The whole call is bound by reading the tokens
 // once (2·D bytes per token): the contraction is 2·N·D FLOP per token, i.e. N FLOP/byte — below
 // the tensor/HBM ridge for every N this supports (≤ 512).
@@ -58,6 +59,22 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// 32 consecutive fp32 TMEM columns of this thread's lane (no wait)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // warp-converged issue: the whole warp runs the loop, one elected lane issues
 __device__ __forceinline__ void mma_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                       uint32_t accumulate) {
@@ -77,13 +94,15 @@ __device__ __forceinline__ void commit_w(uint32_t bar) {
       : "memory");
 }
 
-template <int KMAX>
+// KMAX = K exactly when EXACT (K <= 8), else an upper bound with runtime K (K in 9..16)
+// NB = weight boxes (MMAs) per K step: 1 for N <= 256, 2 above
+template <int KMAX, bool EXACT, int NB>
 __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __grid_constant__ RouterParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
   constexpr int A_BYTES = RBM * RBK * 2;
-  const int B_BYTES = p.n_box * p.box_rows * 128;
+  const int B_BYTES = NB * p.box_rows * 128;
   const int STAGE = A_BYTES + B_BYTES;
   const int S = p.stages;
   uint8_t *sA = smem;
@@ -129,7 +148,8 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __grid_
           const uint32_t fb = smem_u32(full + stage);
           mbar_expect_tx(fb, STAGE);
           tma_load_2d_hint(smem_u32(sA + stage * A_BYTES), &p.tmX, fb, kb * RBK, t * RBM, pol_x);
-          for (int c = 0; c < p.n_box; ++c)
+#pragma unroll
+          for (int c = 0; c < NB; ++c)
             tma_load_2d_hint(smem_u32(sB + stage * B_BYTES + c * p.box_rows * 128), &p.tmW, fb, kb * RBK,
                              c * p.box_rows, pol_w);
           if (++stage == S) {
@@ -161,7 +181,8 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __grid_
         const uint64_t bd = bdesc0 + (uint32_t)((stage * B_BYTES) >> 4);
 #pragma unroll
         for (int kk = 0; kk < RBK / 16; ++kk)
-          for (int c = 0; c < p.n_box; ++c)
+#pragma unroll
+          for (int c = 0; c < NB; ++c)
             mma_w(d_tmem + c * p.box_rows, ad + (uint32_t)(kk * 2),
                   bd + (uint32_t)((c * p.box_rows * 128 + kk * 32) >> 4), idesc, (kb | kk) != 0);
         commit_w(smem_u32(empty + stage));
@@ -192,50 +213,55 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __grid_
         tv[i] = -INFINITY;
         ti[i] = 0;
       }
-      float mx = -INFINITY, last = -INFINITY;
-      // pass 1: max, top-K by logit (softmax is monotone), optional logits copy
-      for (int j = 0; j < N; j += 8) {
-        float v[8];
-        tmem_ld8(taddr + j, v);
+      float mx = -INFINITY, last = -INFINITY, sum = 0.f;
+      // one pass over the logits in 64-column chunks (two x32 TMEM loads, one wait): running max
+      // with the sum rescaled once per chunk (online softmax), and the top-K by logit (softmax is
+      // monotone in z)
+      for (int j = 0; j < N; j += 64) {
+        float v[64];
+        tmem_ld32(taddr + j, v);
+        tmem_ld32(taddr + j + 32, v + 32);
         tmem_ld_wait();
+        float cm = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 64; ++i)
+          if (j + i < N) cm = fmaxf(cm, v[i]);
+        const float nm = fmaxf(mx, cm);
+        sum *= expf(mx - nm);          // 0 on the first chunk (exp(-inf) = 0)
+        mx = nm;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
           const int e = j + i;
           if (e < N) {
-            float z = v[i];
+            const float z = v[i];
             if (p.logits && row_ok) p.logits[row * N + e] = z;
-            mx = fmaxf(mx, z);
+            sum += expf(z - mx);
             if (z > last) {            // strictly greater: an equal later id never displaces
-              int ze = e;
-              bool shift = false;      // below the insertion point every entry moves down one
+              // branch-free insertion into the descending list (positions are compile-time, so
+              // tv / ti stay in registers): entry r takes entry r-1 if z beats that one, else z
+              // if z beats entry r
 #pragma unroll
-              for (int r = 0; r < KMAX; ++r) {
-                if (r < K && (shift || z > tv[r])) {
-                  shift = true;
-                  const float fv = tv[r];
-                  const int fi = ti[r];
-                  tv[r] = z;
-                  ti[r] = ze;
-                  z = fv;
-                  ze = fi;
+              for (int r = KMAX - 1; r >= 1; --r) {
+                if (EXACT || r < K) {
+                  const bool up = z > tv[r - 1], here = z > tv[r];
+                  tv[r] = up ? tv[r - 1] : (here ? z : tv[r]);
+                  ti[r] = up ? ti[r - 1] : (here ? e : ti[r]);
                 }
               }
+              if (z > tv[0]) {
+                tv[0] = z;
+                ti[0] = e;
+              }
+              if (EXACT) {
+                last = tv[KMAX - 1];
+              } else {
 #pragma unroll
-              for (int r = 0; r < KMAX; ++r)
-                if (r == K - 1) last = tv[r];
+                for (int r = 0; r < KMAX; ++r)
+                  if (r == K - 1) last = tv[r];
+              }
             }
           }
         }
-      }
-      // pass 2: Σ_e exp(z_e - max) in expert order
-      float sum = 0.f;
-      for (int j = 0; j < N; j += 8) {
-        float v[8];
-        tmem_ld8(taddr + j, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (j + i < N) sum += expf(v[i] - mx);
       }
       tc_fence_before();
       __syncwarp();
@@ -259,10 +285,14 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __grid_
                  : "memory");
 }
 
-template <int KMAX>
+template <int KMAX, bool EXACT>
 llep_status launch_router(RouterParams &prm, int grid, int smem, cudaStream_t s) {
-  auto kern = router_kernel<KMAX>;
-  LLEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  auto kern = prm.n_box == 1 ? router_kernel<KMAX, EXACT, 1> : router_kernel<KMAX, EXACT, 2>;
+  static int smem_set[2] = {0, 0};
+  if (smem > smem_set[prm.n_box - 1]) {
+    LLEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    smem_set[prm.n_box - 1] = smem;
+  }
   kern<<<grid, kRouterThreads, smem, s>>>(prm);
   LLEP_CUDA(cudaGetLastError());
   return LLEP_OK;
@@ -301,10 +331,17 @@ llep_status run_router(const RouterArgs &a, cudaStream_t s) {
   prm.gates = a.gates;
   prm.logits = a.logits;
   const int grid = (int)(tiles < a.num_sms ? tiles : a.num_sms);
-  if (a.top_k <= 2) return launch_router<2>(prm, grid, smem, s);
-  if (a.top_k <= 4) return launch_router<4>(prm, grid, smem, s);
-  if (a.top_k <= 8) return launch_router<8>(prm, grid, smem, s);
-  return launch_router<16>(prm, grid, smem, s);
+  switch (a.top_k) {
+    case 1: return launch_router<1, true>(prm, grid, smem, s);
+    case 2: return launch_router<2, true>(prm, grid, smem, s);
+    case 3: return launch_router<3, true>(prm, grid, smem, s);
+    case 4: return launch_router<4, true>(prm, grid, smem, s);
+    case 5: return launch_router<5, true>(prm, grid, smem, s);
+    case 6: return launch_router<6, true>(prm, grid, smem, s);
+    case 7: return launch_router<7, true>(prm, grid, smem, s);
+    case 8: return launch_router<8, true>(prm, grid, smem, s);
+    default: return launch_router<16, false>(prm, grid, smem, s);
+  }
 }
 
 }  // namespace llep

@@ -183,6 +183,54 @@ def run_mode(L, shape, rank, local, world, group, inputs, ep: bool, steps: int, 
     return res
 
 
+def run_trace(L, shape, rank, local, world, group, path, steps, warmup):
+    """Row f4 (trace replay): each step replays the next record of a SPEC-format trace (per-device
+    per-expert slot counts -> this rank's routing with exactly those counts), LLEP and EP on one
+    context each.  Returns tokens/s over the replayed steps (max over ranks)."""
+    import torch
+    N, K, D, H, M = shape.n_experts, shape.top_k, shape.d_model, shape.d_ff, shape.experts_per_rank
+    recs = W.load_trace(path, N, world)
+    if not recs:
+        raise SystemExit(f"empty trace {path}")
+    dev = torch.device(f"cuda:{local}")
+    steps_in = []
+    for r, C in enumerate(recs):
+        ids = W.routing_from_counts(C[rank], K, rank, SEED + r)
+        B = ids.shape[0]
+        steps_in.append((B, torch.from_numpy(ids).to(dev),
+                         torch.from_numpy(W.gate_weights(B, K, rank, SEED + r)).to(dev)))
+    bmax = max(max(int(C[p].sum()) // K for C in recs) for p in range(world))
+    x = W.tokens_torch(max(bmax, 1), D, rank, dev, SEED)
+    w13, w2 = W.expert_weights_torch(range(rank * M, (rank + 1) * M), D, H, dev, SEED)
+    out_tokens = sum(int(C.sum()) // K for C in recs)
+    res = {"records": len(recs), "path": os.path.basename(path)}
+    for mode in ("llep", "ep"):
+        ctx = L.Context(N, K, D, H, world, rank, local, max(bmax, 1), group=group)
+        out = torch.empty_like(x)
+
+        def step(i):
+            B, ids, g = steps_in[i % len(recs)]
+            ctx(x[:B], ids, g, w13, w2, ep=(mode == "ep"), out=out[:B])
+
+        for i in range(max(warmup, len(recs))):
+            step(i)
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = max(steps, len(recs))
+        e0.record()
+        for i in range(n):
+            step(i)
+        e1.record()
+        barrier(world)
+        ms = max_over_ranks(e0.elapsed_time(e1), world)
+        ctx.close()
+        tok = sum(int(recs[i % len(recs)].sum()) // K for i in range(n))
+        res[mode] = {"tokens_s": tok / (ms / 1e3), "ms_per_step": ms / n}
+    res["speedup_vs_ep"] = res["ep"]["ms_per_step"] / res["llep"]["ms_per_step"]
+    res["tokens_per_record_all_ranks"] = out_tokens / len(recs)
+    return res
+
+
 def run_backward(L, ctx, shape, inputs, steps, warmup, world, seed):
     """Row f1: prepare + llep_moe_backward per step (recompute + all gradients), CUDA-event timed."""
     import torch
@@ -396,6 +444,8 @@ def gpu_main(args):
         bwd_ms = run_backward(L, ll_ctx, shape, inputs, max(3, args.steps // 2), 3, world, SEED)
     ll_ctx.close()
     router = run_router(L, shape, x, max(10, args.steps), 3)
+    trace = run_trace(L, shape, rank, local, world, group, args.trace, args.steps, args.warmup) \
+        if args.trace else None
 
     sweep = []
     if args.sweep:
@@ -480,6 +530,8 @@ def gpu_main(args):
                                     "dx, dgates, dW13, dW_down incl. spilled-expert gradient return)"}
     router["frac_hbm"] = router["gbs"] / peaks["hbm_gbs"]
     line["router"] = router
+    if trace:
+        line["trace"] = trace
     if e2e:
         line["e2e"] = e2e
     if sweep:
@@ -554,6 +606,8 @@ def main():
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--mem-cap-gb", type=float, default=None,
                     help="per-GPU memory cap (the Q3 'tight memory cap' config): EP reports OOM if its plan does not fit")
+    ap.add_argument("--trace", default=None,
+                    help="also replay a SPEC-format load trace (one record per step), LLEP and EP")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-backward", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -247,3 +247,53 @@ def gate_weights(B: int, K: int, rank: int, seed: int = BASE_SEED) -> np.ndarray
 
 def scenario_name(hot_pct: Optional[int], n_hot: int) -> str:
     return "balanced" if hot_pct is None else f"{hot_pct}pct_into_{n_hot}"
+
+
+# --------------------------------------------------------------------------- trace replay (row f4)
+class TraceError(ValueError):
+    pass
+
+
+def load_trace(path: str, n_experts: int, world: int = 1) -> list:
+    """Per-expert load histograms from a trace file (SPEC's format): one record per line,
+    comma-separated: a record id, then N (global l) or P·N (per-device counts, device-major)
+    non-negative integers.  Blank lines and lines starting with '#' are skipped.  Returns one
+    [world, N] int64 load matrix per record; a reduced (N-entry) record puts all load on device 0
+    (planner-only use).  Malformed records, negative counts and width mismatches raise
+    TraceError naming the line."""
+    out = []
+    with open(path) as f:
+        for ln, line in enumerate(f, 1):
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            fields = [v.strip() for v in line.split(",")]
+            try:
+                vals = [int(v) for v in fields[1:]]
+            except ValueError as e:
+                raise TraceError(f"{path}:{ln}: malformed record ({e})") from None
+            if any(v < 0 for v in vals):
+                raise TraceError(f"{path}:{ln}: negative count")
+            if len(vals) == n_experts:
+                C = np.zeros((world, n_experts), dtype=np.int64)
+                C[0] = vals
+            elif len(vals) == world * n_experts:
+                C = np.asarray(vals, dtype=np.int64).reshape(world, n_experts)
+            else:
+                raise TraceError(f"{path}:{ln}: {len(vals)} counts, expected N={n_experts} "
+                                 f"or P*N={world * n_experts}")
+            out.append(C)
+    return out
+
+
+def routing_from_counts(counts, top_k: int, rank: int, seed: int = BASE_SEED) -> np.ndarray:
+    """topk_ids [B, K] int32 whose slot multiset is exactly `counts` (one device's row of a trace
+    record; Σ counts must be a multiple of K), Fisher-Yates shuffled with PCG64(seed, rank)."""
+    counts = np.asarray(counts, dtype=np.int64)
+    S = int(counts.sum())
+    if S % top_k:
+        raise TraceError(f"{S} routed slots are not a multiple of top-K={top_k}")
+    rng = np.random.Generator(np.random.PCG64([seed & M32, rank, 0x7ACE]))
+    ids = np.repeat(np.arange(len(counts), dtype=np.int64), counts)
+    rng.shuffle(ids)
+    return ids.astype(np.int32).reshape(S // top_k, top_k)

@@ -252,3 +252,28 @@ def test_inconsistent_plan_rejected(L):
     assert ei.value.code == 2
     ctx.forward(x, ids, gates, w13, w2, good)   # the prepared plan still works
     ctx.close()
+
+
+def test_layer_trace_replay(L, tmp_path):
+    """Row f4 (trace replay): one context replays three trace records (SPEC format) with different
+    batch sizes and skews; each step's output vs O3 on that record's routing."""
+    N, K, D, H = 8, 2, 256, 512
+    f = tmp_path / "trace.csv"
+    f.write_text("a,100,100,100,100,100,100,100,100\n"       # balanced, 400 tokens
+                 "b,1500,10,10,10,10,10,0,0\n"             # one hot expert, 775 tokens
+                 "c,0,0,0,0,0,0,0,6\n")                    # everything on the last expert, 3 tokens
+    recs = W.load_trace(str(f), N, world=1)
+    ctx = L.Context(N, K, D, H, 1, 0, 0, 1024)
+    seed = 21
+    w13, w2 = W.expert_weights_torch(range(N), D, H, "cuda", seed)
+    x_all = W.tokens_torch(1024, D, 0, "cuda", seed)
+    for rec in recs:
+        ids_np = W.routing_from_counts(rec[0], K, 0, seed)
+        B = ids_np.shape[0]
+        g_np = W.gate_weights(B, K, 0, seed)
+        out = ctx(x_all[:B].contiguous(), torch.from_numpy(ids_np).cuda(), torch.from_numpy(g_np).cuda(), w13, w2)
+        torch.cuda.synchronize()
+        ref = LC.oracle_rank_output(W.LayerShape(N, K, D, H, B, 1), 0, ids_np, g_np, seed)
+        mr, l2 = LC.errors(_to_np(out), ref)
+        assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (rec, mr, l2)
+    ctx.close()

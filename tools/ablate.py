@@ -1,0 +1,137 @@
+"""Row f3: the paper's ablations (§5.3 F-abl1/F-abl2, App. B F-nexp) on one B200 by critical-rank
+emulation, next to the paper's 8×H200 layer speedups.
+
+Every ablation point is the F-head layer (N=128, K=4, D=H=2048, 32K tokens per GPU, P=8, 4 hot
+experts; D7) with one parameter varied, λ=1.3, α=1, m=1024 unless varied:
+  batch   B per GPU ∈ {4K, 8K, 16K, 32K, 64K}            hot ∈ {30, 50, 80, 95} %
+  alpha   α ∈ {1.0, 1.5, 2.0, 2.5, 3.0}                  hot ∈ {30, 50, 80, 95} %
+  lambda  λ ∈ {1.1, 1.4, 1.7, 2.0, 2.3, 2.6}, B = 8K     hot ∈ {15, 20, 30, 50} %
+  hidden  D = H ∈ {512, 1024, 2048, 4096}                hot ∈ {30, 50, 80, 95} %
+  experts N ∈ {16, 32, 64, 128, 256}                     hot ∈ {30, 50, 80, 95} %
+
+For each point the plans of all 8 ranks are computed (host planner == device planner), the most
+loaded rank's grouped GEMM1 + GEMM2 are timed on this GPU for EP and for LLEP (alternating, median),
+and three numbers are printed: `gemm_speedup` (measured), `row_bound` (max EP rows / max LLEP rows),
+and `modeled_speedup` = (EP GEMM + EP link) / (LLEP GEMM + LLEP link), where link time is MODELLED,
+not measured: dispatch + combine bytes of the busiest device (2D+4 and 2D bytes per remote row) and
+the weight broadcast (6·D·H bytes per tree round, ⌈log2(replicas+1)⌉ rounds per spilled expert,
+serialised per source device) over NVLink 5 at 900 GB/s per direction.
+
+    python tools/ablate.py [--which batch,alpha,lambda,hidden,experts] [--reps 3] > out.jsonl
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+from emulate_p8 import Gemms, rank_groups  # noqa: E402
+from paper_2601_17111_b200 import llep as L  # noqa: E402
+from synth import workload as W  # noqa: E402
+
+NVLINK = 900e9
+P = 8
+PAPER = {   # speedups read from the paper's plots (8×H200, whole layer)
+    "batch": {30: [0.66, 0.99, 1.39, 1.81, 2.24], 50: [0.89, 1.33, 2.00, 2.64, 3.18],
+              80: [1.15, 1.84, 2.78, 3.78, 4.73], 95: [1.29, 2.09, 3.23, 4.29, 5.46]},
+    "alpha": {30: [1.75, 1.56, 1.28, 1.10, 0.98], 50: [2.57, 2.16, 1.83, 1.58, 1.38],
+              80: [3.66, 3.10, 2.71, 2.29, 1.99], 95: [4.19, 3.51, 3.09, 2.67, 2.32]},
+    "lambda": {15: [0.70, 0.69, 0.70, 1.06, 1.07, 1.07], 20: [0.73, 0.74, 0.74, 0.73, 1.04, 1.04],
+               30: [0.89, 0.88, 0.90, 0.88, 0.89, 0.90], 50: [1.21, 1.22, 1.21, 1.21, 1.21, 1.22]},
+    "hidden": {30: [0.80, 1.21, 1.71, 2.24], 50: [1.06, 1.70, 2.43, 3.36],
+               80: [1.47, 2.36, 3.54, 4.93], 95: [1.67, 2.69, 4.03, 5.73]},
+    "experts": {30: [0.61, 1.03, 1.69, 1.81, 1.94], 50: [1.24, 1.48, 2.05, 2.5, 2.8],
+                80: [1.76, 2.23, 2.92, 3.61, 4.04], 95: [1.94, 2.6, 3.38, 4.06, 4.57]},
+}
+GRID = {"batch": [4096, 8192, 16384, 32768, 65536], "alpha": [1.0, 1.5, 2.0, 2.5, 3.0],
+        "lambda": [1.1, 1.4, 1.7, 2.0, 2.3, 2.6], "hidden": [512, 1024, 2048, 4096],
+        "experts": [16, 32, 64, 128, 256]}
+
+
+def link_seconds(plan, cnt, D, H, M):
+    """Modelled NVLink time of one layer: dispatch + combine rows and the weight broadcast."""
+    egress = np.zeros(P)
+    ingress = np.zeros(P)
+    for e, chunks in enumerate(plan.chunks):
+        c = int(cnt[e])
+        for (d, s, t) in chunks:
+            for p in range(P):   # rows of expert e from source rank p: global range [p·c, (p+1)·c)
+                n = max(0, min(t, (p + 1) * c) - max(s, p * c))
+                if n and p != d:
+                    egress[p] += n * (2 * D + 4 + 2 * D)
+                    ingress[d] += n * (2 * D + 4 + 2 * D)
+    t_rows = max(egress.max(), ingress.max()) / NVLINK
+    reps = {}
+    for (e, src, dst) in plan.transfers:
+        reps.setdefault(e, []).append(dst)
+    wsrc = np.zeros(P)
+    for e, ds in reps.items():
+        wsrc[e // M] += math.ceil(math.log2(len(ds) + 1)) * 6 * D * H
+    return t_rows + wsrc.max() / NVLINK
+
+
+def point(N, K, D, H, B, alpha, lam, hot, nhot, reps):
+    sh = W.LayerShape(N, K, D, H, B, P)
+    M = N // P
+    cnt = W.slot_counts(N, B * K, hot, nhot)
+    loads = (cnt * P).tolist()
+    res, g = {}, {}
+    for mode in ("ep", "llep"):
+        plan = L.plan_host(loads, P, alpha, 1024, lam, ep=(mode == "ep"))
+        per_rank = [sum(rank_groups(plan, r, M)) for r in range(P)]
+        crit = int(np.argmax(per_rank))
+        rows = rank_groups(plan, crit, M)
+        g[mode] = Gemms(rows, D, H)
+        res[mode] = {"rows": int(sum(rows)), "transfers": len(plan.transfers), "fallback": plan.fallback,
+                     "link_ms": 1e3 * link_seconds(plan, cnt, D, H, M), "ms": []}
+    for m in ("ep", "llep"):
+        g[m].run_ms()
+    for _ in range(reps):
+        for m in ("ep", "llep"):
+            res[m]["ms"].append(g[m].run_ms())
+    del g
+    torch.cuda.empty_cache()
+    for m in ("ep", "llep"):
+        res[m]["gemm_ms"] = statistics.median(res[m].pop("ms"))
+    res["gemm_speedup"] = res["ep"]["gemm_ms"] / res["llep"]["gemm_ms"]
+    res["row_bound"] = res["ep"]["rows"] / res["llep"]["rows"]
+    res["modeled_speedup"] = ((res["ep"]["gemm_ms"] + res["ep"]["link_ms"]) /
+                              (res["llep"]["gemm_ms"] + res["llep"]["link_ms"]))
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--which", default="batch,alpha,lambda,hidden,experts")
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    for which in args.which.split(","):
+        for hot, paper in PAPER[which].items():
+            for i, v in enumerate(GRID[which]):
+                N, K, D, H, B, alpha, lam = 128, 4, 2048, 2048, 32768, 1.0, 1.3
+                if which == "batch":
+                    B = v
+                elif which == "alpha":
+                    alpha = v
+                elif which == "lambda":
+                    lam, B = v, 8192
+                elif which == "hidden":
+                    D = H = v
+                else:
+                    N = v
+                r = point(N, K, D, H, B, alpha, lam, hot, 4, args.reps)
+                r.update({"ablation": which, "x": v, "hot_pct": hot, "n_hot": 4, "paper_speedup": paper[i],
+                          "shape": {"N": N, "K": K, "D": D, "H": H, "B_per_gpu": B, "P": P,
+                                    "alpha": alpha, "lambda": lam, "m": 1024}})
+                print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()

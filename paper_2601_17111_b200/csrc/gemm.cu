@@ -85,6 +85,7 @@ __device__ __forceinline__ uint32_t instr_desc() {
 
 struct TileInfo {
   int row0, row_end, nb, wslot, small;
+  int half;   // pair kernel: <= 128 rows left in this block -> M=128 pair MMA (64 rows per CTA)
 };
 
 template <int TM = BM>
@@ -114,6 +115,7 @@ __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int *
   ti.row_end = g.row_base + g.n_rows;
   ti.wslot = g.wslot;
   ti.small = g.n_rows <= kSmallGroupRows;  // its weights are streamed once: evict first from L2
+  ti.half = ti.row_end - ti.row0 <= TM / 2;
   return ti;
 }
 
@@ -328,12 +330,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
 // CTAs' TMA loads complete on the leader's full barrier; the MMA commits are multicast to both
 // CTAs' empty / accumulator-full barriers; each CTA's epilogue drains its own TMEM lanes (its 128
 // rows of the 256-row accumulator) and arrives on the leader's TMEM-empty barrier.
-template <int BN, int KSUB = 1>   // KSUB: 64-deep K sub-tiles per pipeline stage
+// SwiGLU exchange buffer of a half tile (mode 0): [64 rows][S0+1] + [64 rows][S1+1] fp32 (odd strides)
+constexpr int kXchgBytes = 64 * (65 + 65) * 4;   // S0, S1 <= 64 for BN <= 256
+
+template <int BN, int KSUB = 1, int XB = 0>   // KSUB: 64-deep K sub-tiles per stage; XB: exchange bytes
 struct Cfg2 {
   static constexpr int A_BYTES = BM * BK * 2 * KSUB;
   static constexpr int B_BYTES = (BN / 2) * BK * 2 * KSUB;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int EXTRA = 1024 + 256;
+  static constexpr int EXTRA = 1024 + 256 + XB;
   static constexpr int STAGES_RAW = (kSmemBudget - EXTRA) / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int SMEM = STAGES * STAGE + EXTRA;
@@ -412,7 +417,7 @@ __device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
 
 template <int BN, int MODE, int KSUB>
 __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(const __grid_constant__ GemmParams p) {
-  using C = Cfg2<BN, KSUB>;
+  using C = Cfg2<BN, KSUB, MODE == 0 ? kXchgBytes : 0>;
   constexpr int KST = BK * KSUB;                 // K per pipeline stage
   constexpr int S = C::STAGES;
   constexpr int TM = 2 * BM;                     // rows per pair tile
@@ -425,6 +430,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S * C::STAGE);
   uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+  float *xchg = reinterpret_cast<float *>(smem + S * C::STAGE + 256);   // mode 0 half tiles
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
@@ -487,7 +493,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
           const uint32_t fb = mapa_shared(fl, 0);
           for (int s2 = 0; s2 < nsub; ++s2) {
             tma_load_2d_pair(smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128)), &p.tmA, fb,
-                             (kb * KSUB + s2) * BK, ti.row0 + (int)crank * BM, pol_act);
+                             (kb * KSUB + s2) * BK, ti.row0 + (int)crank * (ti.half ? BM / 2 : BM), pol_act);
             tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES + s2 * ((BN / 2) * 128)), wm, fb,
                              (kb * KSUB + s2) * BK, brow, ti.small ? pol_first : pol_last);
           }
@@ -501,8 +507,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
   } else if (warp == 1) {
     if (leader) {
       // ---------------------------------------------------------------- MMA issuer (leader warp)
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                             ((uint32_t)(TM >> 4) << 24);
+      // M=256 for a full pair tile, M=128 (64 rows per CTA) when <= 128 rows of the block remain
+      const uint32_t idesc_full = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                  ((uint32_t)(TM >> 4) << 24);
+      const uint32_t idesc_half = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                  ((uint32_t)((TM / 2) >> 4) << 24);
       const uint64_t adesc0 = smem_desc(smem_u32(sA)), bdesc0 = smem_desc(smem_u32(sB));
       int stage = 0;
       uint32_t phase = 0;
@@ -510,6 +519,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       for (int t = pair; t < total_tiles; t += n_pairs, ++it) {
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
+        const TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
+        const uint32_t idesc = ti.half ? idesc_half : idesc_full;
         mbar_wait(smem_u32(tempty + acc), aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
@@ -555,7 +566,104 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
       const int col0 = ti.nb * BNO;
       constexpr int bno = BNO;
-      if (MODE == 2) {
+      if (ti.half) {
+        // M=128 pair tile: this CTA's 64 rows.  TMEM lanes 0-63 hold accumulator columns [0, BN/2)
+        // (the B rows staged by CTA 0) and lanes 64-127 columns [BN/2, BN) (CTA 1's) of the SAME
+        // 64 rows, both at TMEM columns 0 .. BN/2-1.
+        constexpr int BH = BN / 2;
+        const int L = q * 32 + lane, hi = L >> 6, r = L & 63;
+        const int hrow = ti.row0 + (int)crank * (BM / 2) + r;
+        const bool hok = hrow < ti.row_end;
+        if (MODE == 1) {
+          const float gs = hok ? p.gate[hrow] : 0.f;
+          __nv_bfloat16 *orow = p.out + (size_t)hrow * p.nout + col0 + hi * BH;
+          if (p.peer_slot && hok) {
+            const int32_t src = p.row_src[hrow];
+            orow = reinterpret_cast<__nv_bfloat16 *>(p.peer_slot[src & 31]) + (size_t)(src >> 5) * p.nout +
+                   col0 + hi * BH;
+          }
+#pragma unroll 1
+          for (int j = 0; j < BH; j += 8) {
+            float v[8];
+            tmem_ld8(taddr + j, v);
+            tmem_ld_wait();
+            if (hok && col0 + hi * BH + j < p.nout) {
+              uint4 o;
+              __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(gs * v[2 * i], gs * v[2 * i + 1]);
+              *reinterpret_cast<uint4 *>(orow + j) = o;
+            }
+          }
+        } else if (MODE == 2) {
+          // lanes 0-63 hold gate pre-activations, lanes 64-127 up: GU[r] = [g (nout) | u (nout)]
+          __nv_bfloat16 *dst = p.out + (size_t)hrow * 2 * p.nout + hi * p.nout + col0;
+#pragma unroll 1
+          for (int j = 0; j < BH; j += 8) {
+            float v[8];
+            tmem_ld8(taddr + j, v);
+            tmem_ld_wait();
+            if (hok && col0 + j < p.nout) {
+              uint4 o;
+              __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+              *reinterpret_cast<uint4 *>(dst + j) = o;
+            }
+          }
+        } else {
+          // SwiGLU needs g (lanes 0-63) and u (lanes 64-127) of the same row: exchange through
+          // shared memory.  Gate lanes finish columns [0, S0), up lanes [S0, BH).
+          constexpr int S0 = (BH / 2 + 7) / 8 * 8, S1 = BH - S0;
+          float *xu = xchg;                          // [64][S0+1] up values of columns [0, S0)
+          float *xg = xchg + 64 * (S0 + 1);          // [64][S1+1] gate values of columns [S0, BH)
+          asm volatile("bar.sync 1, 128;" ::: "memory");   // the previous half tile's reads are done
+          if (hi == 0) {
+#pragma unroll 1
+            for (int j = S0; j < BH; j += 8) {
+              float v[8];
+              tmem_ld8(taddr + j, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 8; ++i) xg[r * (S1 + 1) + (j - S0) + i] = v[i];
+            }
+          } else {
+#pragma unroll 1
+            for (int j = 0; j < S0; j += 8) {
+              float v[8];
+              tmem_ld8(taddr + j, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 8; ++i) xu[r * (S0 + 1) + j + i] = v[i];
+            }
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          __nv_bfloat16 *orow = p.out + (size_t)hrow * p.nout + col0;
+          const int j0 = hi == 0 ? 0 : S0, j1 = hi == 0 ? S0 : BH;
+#pragma unroll 1
+          for (int j = j0; j < j1; j += 8) {
+            float v[8], g[8], u[8];
+            tmem_ld8(taddr + j, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              g[i] = hi == 0 ? v[i] : xg[r * (S1 + 1) + (j - S0) + i];
+              u[i] = hi == 0 ? xu[r * (S0 + 1) + j + i] : v[i];
+            }
+            if (hok && col0 + j < p.nout) {
+              uint4 o;
+              __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float a0 = __fdividef(g[2 * i], 1.f + __expf(-g[2 * i])) * u[2 * i];
+                const float a1 = __fdividef(g[2 * i + 1], 1.f + __expf(-g[2 * i + 1])) * u[2 * i + 1];
+                h[i] = __floats2bfloat162_rn(a0, a1);
+              }
+              *reinterpret_cast<uint4 *>(orow + j) = o;
+            }
+          }
+        }
+      } else if (MODE == 2) {
         // raw gate / up pre-activations for the backward recompute: GU[r] = [g (nout) | u (nout)]
         __nv_bfloat16 *grow = p.out + (size_t)row * 2 * p.nout + col0;
 #pragma unroll 1
@@ -690,7 +798,7 @@ llep_status launch(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
 
 template <int BN, int MODE, int KSUB = 2>
 llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
-  using C = Cfg2<BN, KSUB>;
+  using C = Cfg2<BN, KSUB, MODE == 0 ? kXchgBytes : 0>;
   auto kern = grouped_gemm_2cta_kernel<BN, MODE, KSUB>;
   static bool attr_set = false;
   if (!attr_set) {

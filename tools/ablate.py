@@ -12,10 +12,12 @@ experts; D7) with one parameter varied, λ=1.3, α=1, m=1024 unless va
 For each point the plans of all 8 ranks are computed (host planner == device planner), the most
 loaded rank's grouped GEMM1 + GEMM2 are timed on this GPU for EP and for LLEP (alternating, median),
 and three numbers are printed: `gemm_speedup` (measured), `row_bound` (max EP rows / max LLEP rows),
-and `modeled_speedup` = (EP GEMM + EP link) / (LLEP GEMM + LLEP link), where link time is MODELLED,
-not measured: dispatch + combine bytes of the busiest device (2D+4 and 2D bytes per remote row) and
-the weight broadcast (6·D·H bytes per tree round, ⌈log2(replicas+1)⌉ rounds per spilled expert,
-serialised per source device) over NVLink 5 at 900 GB/s per direction.
+and `modeled_speedup` = (EP GEMM + EP link) / (LLEP GEMM + LLEP link), where the link time is
+MODELLED, not measured: dispatch + combine bytes of the busiest device (2D+4 and 2D bytes per remote
+row) and the weight broadcast (6·D·H bytes per tree round, ⌈log2(replicas+1)⌉ rounds per spilled
+expert, serialised per source device) over NVLink 5 at 900 GB/s per direction.  Timing is steady
+state: each mode runs back to back for >= 150 ms per round (the GPU is power-capped, and a short
+burst after idle runs at ramping clocks), rounds alternate EP / LLEP, median of all iterations.
 
     python tools/ablate.py [--which batch,alpha,lambda,hidden,experts] [--reps 3] > out.jsonl
 """
@@ -25,6 +27,7 @@ import math
 import os
 import statistics
 import sys
+import time
 
 import numpy as np
 import torch
@@ -38,6 +41,7 @@ from synth import workload as W  # noqa: E402
 
 NVLINK = 900e9
 P = 8
+BURST_MS = 150.0
 PAPER = {   # speedups read from the paper's plots (8×H200, whole layer)
     "batch": {30: [0.66, 0.99, 1.39, 1.81, 2.24], 50: [0.89, 1.33, 2.00, 2.64, 3.18],
               80: [1.15, 1.84, 2.78, 3.78, 4.73], 95: [1.29, 2.09, 3.23, 4.29, 5.46]},
@@ -93,9 +97,14 @@ def point(N, K, D, H, B, alpha, lam, hot, nhot, reps):
                      "link_ms": 1e3 * link_seconds(plan, cnt, D, H, M), "ms": []}
     for m in ("ep", "llep"):
         g[m].run_ms()
+    # steady state: each mode runs back to back for >= BURST_MS per round (clocks settle under the
+    # power cap), rounds alternate EP / LLEP, every iteration is CUDA-event timed, median over all
     for _ in range(reps):
         for m in ("ep", "llep"):
-            res[m]["ms"].append(g[m].run_ms())
+            t0, n = time.perf_counter(), 0
+            while n < 3 or (time.perf_counter() - t0) * 1e3 < BURST_MS:
+                res[m]["ms"].append(g[m].run_ms())
+                n += 1
     del g
     torch.cuda.empty_cache()
     for m in ("ep", "llep"):
@@ -110,7 +119,7 @@ def point(N, K, D, H, B, alpha, lam, hot, nhot, reps):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="batch,alpha,lambda,hidden,experts")
-    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--reps", type=int, default=2)
     args = ap.parse_args()
     for which in args.which.split(","):
         for hot, paper in PAPER[which].items():

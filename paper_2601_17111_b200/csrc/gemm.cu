@@ -883,11 +883,13 @@ __device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr) {
 
 struct BwdTile {
   int row0, row_end, m0, n0, g, nk, split, nsplit;
+  int half;   // pair kernel, kind 0: <= 128 rows left in the block -> M=128 pair MMA
 };
 
 template <int KIND>
 __device__ __forceinline__ BwdTile decode_bwd(int t, const BwdParams &p, const int *s_mblk) {
   BwdTile ti;
+  ti.half = 0;
   if (KIND == 0) {
     const int mb = t / p.n_nt;
     ti.n0 = (t - mb * p.n_nt) * kBwdBN;
@@ -923,9 +925,11 @@ __device__ __forceinline__ BwdTile decode_bwd(int t, const BwdParams &p, const i
     const Group g = p.groups[ti.g];
     ti.nsplit = wgrad_splits(g.n_rows, per, p.num_sms);
     const int ks = wgrad_split_rows(g.n_rows, ti.nsplit);
-    const int padded = (g.n_rows + 255) / 256 * 256;
+    // contract only up to the group's last 64-row K block (rows past n_rows are zero in both
+    // operands): a 52-row group costs one K step, not four
+    const int kend = (g.n_rows + BK - 1) / BK * BK;
     const int k0 = ti.split * ks;
-    const int k1 = min(padded, k0 + ks);
+    const int k1 = min(kend, k0 + ks);
     ti.row0 = g.row_base + k0;
     ti.row_end = g.row_base + g.n_rows;
     ti.nk = (k1 - k0) / BK;     // padded rows are zero in both operands
@@ -1167,6 +1171,7 @@ template <int KIND> struct BwdPairCfg {
 template <int KIND>
 __device__ __forceinline__ BwdTile decode_bwd_pair(int t, const BwdParams &p, const int *s_mblk) {
   BwdTile ti;
+  ti.half = 0;
   if (KIND == 0) {
     const int mb = t / p.n_nt;
     ti.n0 = (t - mb * p.n_nt) * kBwdBN;
@@ -1182,6 +1187,7 @@ __device__ __forceinline__ BwdTile decode_bwd_pair(int t, const BwdParams &p, co
     ti.row_end = g.row_base + g.n_rows;
     ti.m0 = 0;
     ti.nk = (p.kdim + BK - 1) / BK;
+    ti.half = ti.row_end - ti.row0 <= BM;
   } else {
     const int per = p.n_mt * p.n_nt;
     int lo = 0, hi = p.n_groups - 1;
@@ -1200,9 +1206,11 @@ __device__ __forceinline__ BwdTile decode_bwd_pair(int t, const BwdParams &p, co
     const Group g = p.groups[ti.g];
     ti.nsplit = wgrad_splits(g.n_rows, per, p.num_sms);
     const int ks = wgrad_split_rows(g.n_rows, ti.nsplit);
-    const int padded = (g.n_rows + 255) / 256 * 256;
+    // contract only up to the group's last 64-row K block (rows past n_rows are zero in both
+    // operands): a 52-row group costs one K step, not four
+    const int kend = (g.n_rows + BK - 1) / BK * BK;
     const int k0 = ti.split * ks;
-    const int k1 = min(padded, k0 + ks);
+    const int k1 = min(kend, k0 + ks);
     ti.row0 = g.row_base + k0;
     ti.row_end = g.row_base + g.n_rows;
     ti.nk = (k1 - k0) / BK;
@@ -1291,7 +1299,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
           const uint32_t a_dst = smem_u32(sA + stage * kPairA);
           const uint32_t b_dst = smem_u32(sB + stage * kPairB);
           if (KIND == 0) {
-            tma_load_2d_pair(a_dst, &p.tmA, fb, kb * BK, ti.row0 + (int)crank * BM, pol);
+            tma_load_2d_pair(a_dst, &p.tmA, fb, kb * BK, ti.row0 + (int)crank * (ti.half ? BM / 2 : BM), pol);
 #pragma unroll
             for (int c = 0; c < 2; ++c)
               tma_load_2d_pair(b_dst + c * 8192, bm, fb, ti.n0 + (int)crank * 128 + c * 64, wrow + kb * BK, pol);
@@ -1312,13 +1320,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((KIND == 1 ? 1u : 0u) << 15) |
-                             (1u << 16) | ((uint32_t)(kBwdBN >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
+      const uint32_t idesc_full = (1u << 4) | (1u << 7) | (1u << 10) | ((KIND == 1 ? 1u : 0u) << 15) |
+                                  (1u << 16) | ((uint32_t)(kBwdBN >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
+      const uint32_t idesc_half = (idesc_full & ~(0x1Fu << 24)) | ((uint32_t)(BM >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int t = pair; t < total_tiles; t += n_pairs, ++it) {
         const BwdTile ti = decode_bwd_pair<KIND>(t, p, s_mblk);
+        const uint32_t idesc = (KIND == 0 && ti.half) ? idesc_half : idesc_full;
         const int acc = it & 1;
         mbar_wait(smem_u32(tempty + acc), ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -1352,15 +1362,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
       if (KIND == 0) {
-        const int row = ti.row0 + (int)crank * BM + q * 32 + lane;
+        // full tile: lane = row of this CTA's 128; half tile (M=128 pair MMA): lanes 0-63 hold
+        // columns [0, 128) and lanes 64-127 columns [128, 256) of the CTA's 64 rows
+        const int L = q * 32 + lane;
+        const int row = ti.half ? ti.row0 + (int)crank * (BM / 2) + (L & 63) : ti.row0 + (int)crank * BM + L;
+        const int c0 = ti.half ? (L >> 6) * (kBwdBN / 2) : 0, cw = ti.half ? kBwdBN / 2 : kBwdBN;
         const bool ok = row < ti.row_end;
-        __nv_bfloat16 *orow = reinterpret_cast<__nv_bfloat16 *>(p.out) + (size_t)row * p.nout + ti.n0;
+        __nv_bfloat16 *orow = reinterpret_cast<__nv_bfloat16 *>(p.out) + (size_t)row * p.nout + ti.n0 + c0;
 #pragma unroll 1
-        for (int j = 0; j < kBwdBN; j += 8) {
+        for (int j = 0; j < cw; j += 8) {
           float v[8];
           tmem_ld8(taddr + j, v);
           tmem_ld_wait();
-          if (ok && ti.n0 + j < p.nout) {
+          if (ok && ti.n0 + c0 + j < p.nout) {
             uint4 o;
             __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
 #pragma unroll

@@ -123,7 +123,7 @@ def test_gemm_bwd(L, kind, kdim, nout, pair):
     """Backward GEMMs with MN-major UMMA operands vs a plain fp32 torch reference."""
     g = torch.Generator(device="cuda").manual_seed(kind * 100 + kdim + nout)
     E = 3
-    sizes = [1, 300, 129, 600, 256] + ([9000] if kind == 1 else [])   # 9000 rows: split-K path
+    sizes = [1, 300, 129, 600, 256, 64, 65, 128] + ([9000] if kind == 1 else [])   # 9000 rows: split-K path
     groups, rb = [], 0
     for i, n in enumerate(sizes):
         groups.append((i % E, rb, n))

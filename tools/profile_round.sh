@@ -13,4 +13,6 @@ ncu --set full --clock-control none --import-source on --kernel-name-base mangle
     -k regex:"dispatch|combine|planner|layout" -s 24 -c 4 -o gpurun_out/prof_route_${R} $B --no-backward > /dev/null 2>&1
 ncu --set full --clock-control none --kernel-name-base mangled \
     -k regex:gemm_bwd -s 4 -c 4 -o gpurun_out/prof_bwd_${R} $B > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
+    -k regex:router -s 3 -c 1 -o gpurun_out/prof_router_${R} python tools/router_bench.py g120 > /dev/null 2>&1
 ls -la gpurun_out/

@@ -35,11 +35,10 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tools"))
-from emulate_p8 import Gemms, rank_groups  # noqa: E402
+from emulate_p8 import Gemms, link_seconds, rank_groups  # noqa: E402
 from paper_2601_17111_b200 import llep as L  # noqa: E402
 from synth import workload as W  # noqa: E402
 
-NVLINK = 900e9
 P = 8
 BURST_MS = 150.0
 PAPER = {   # speedups read from the paper's plots (8×H200, whole layer)
@@ -57,28 +56,6 @@ PAPER = {   # speedups read from the paper's plots (8×H200, whole layer)
 GRID = {"batch": [4096, 8192, 16384, 32768, 65536], "alpha": [1.0, 1.5, 2.0, 2.5, 3.0],
         "lambda": [1.1, 1.4, 1.7, 2.0, 2.3, 2.6], "hidden": [512, 1024, 2048, 4096],
         "experts": [16, 32, 64, 128, 256]}
-
-
-def link_seconds(plan, cnt, D, H, M):
-    """Modelled NVLink time of one layer: dispatch + combine rows and the weight broadcast."""
-    egress = np.zeros(P)
-    ingress = np.zeros(P)
-    for e, chunks in enumerate(plan.chunks):
-        c = int(cnt[e])
-        for (d, s, t) in chunks:
-            for p in range(P):   # rows of expert e from source rank p: global range [p·c, (p+1)·c)
-                n = max(0, min(t, (p + 1) * c) - max(s, p * c))
-                if n and p != d:
-                    egress[p] += n * (2 * D + 4 + 2 * D)
-                    ingress[d] += n * (2 * D + 4 + 2 * D)
-    t_rows = max(egress.max(), ingress.max()) / NVLINK
-    reps = {}
-    for (e, src, dst) in plan.transfers:
-        reps.setdefault(e, []).append(dst)
-    wsrc = np.zeros(P)
-    for e, ds in reps.items():
-        wsrc[e // M] += math.ceil(math.log2(len(ds) + 1)) * 6 * D * H
-    return t_rows + wsrc.max() / NVLINK
 
 
 def point(N, K, D, H, B, alpha, lam, hot, nhot, reps):

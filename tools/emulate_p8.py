@@ -4,7 +4,8 @@ For a scenario of the G120 layer (N=128, K=4, D=H=2880, 32K tokens per rank, P=8
 ranks are computed from the synthetic routing (host planner, bit-identical to the device one); for
 standard EP and for LLEP the most loaded rank's expert groups (rows per expert, in the layout
 kernel's order) are built and that rank's two grouped GEMMs are timed on this GPU through the C ABI
-(2-CTA kernels, CUDA events, median of several runs).  The GEMMs are ~93 % of a layer step at P=1;
+(2-CTA kernels, CUDA events; steady state: each mode runs back to back for >= 150 ms per round,
+rounds alternate, median of all iterations).  The GEMMs are ~93 % of a layer step at P=1;
 dispatch / combine / weight-broadcast costs over NVLink are NOT measured here.
 
     python tools/emulate_p8.py [--scenarios 95:1,80:1,...] [--reps 5]
@@ -14,6 +15,9 @@ import json
 import os
 import statistics
 import sys
+import time
+
+import math
 
 import numpy as np
 import torch
@@ -22,6 +26,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2601_17111_b200 import llep as L  # noqa: E402
 from synth import workload as W  # noqa: E402
+
+NVLINK = 900e9   # NVLink 5, per direction (modelled link time only)
 
 
 def rank_groups(plan, rank, M):
@@ -35,6 +41,28 @@ def rank_groups(plan, rank, M):
             if r:
                 rows.append(r)
     return rows
+
+
+def link_seconds(plan, cnt, D, H, M, P=8):
+    """Modelled NVLink time of one layer: dispatch + combine rows and the weight broadcast."""
+    egress = np.zeros(P)
+    ingress = np.zeros(P)
+    for e, chunks in enumerate(plan.chunks):
+        c = int(cnt[e])
+        for (d, s, t) in chunks:
+            for p in range(P):   # rows of expert e from source rank p: global range [p·c, (p+1)·c)
+                n = max(0, min(t, (p + 1) * c) - max(s, p * c))
+                if n and p != d:
+                    egress[p] += n * (2 * D + 4 + 2 * D)
+                    ingress[d] += n * (2 * D + 4 + 2 * D)
+    t_rows = max(egress.max(), ingress.max()) / NVLINK
+    reps = {}
+    for (e, src, dst) in plan.transfers:
+        reps.setdefault(e, []).append(dst)
+    wsrc = np.zeros(P)
+    for e, ds in reps.items():
+        wsrc[e // M] += math.ceil(math.log2(len(ds) + 1)) * 6 * D * H
+    return t_rows + wsrc.max() / NVLINK
 
 
 class Gemms:
@@ -69,7 +97,7 @@ def main():
     ap.add_argument("--config", default="g120")
     ap.add_argument("--world", type=int, default=8)
     ap.add_argument("--scenarios", default="95:1,80:1,50:1,30:1,95:4,95:16,0:0")
-    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--reps", type=int, default=2)
     args = ap.parse_args()
     base = W.CONFIGS[args.config]
     P = args.world
@@ -90,18 +118,27 @@ def main():
             rows = rank_groups(plan, crit, M)
             g[mode] = Gemms(rows, sh.d_model, sh.d_ff)
             res[mode] = {"critical_rank": crit, "rows": int(sum(rows)), "groups": len(rows),
-                         "transfers": len(plan.transfers), "fallback": plan.fallback, "ms": []}
+                         "transfers": len(plan.transfers), "fallback": plan.fallback,
+                         "link_ms_modelled": 1e3 * link_seconds(plan, cnt, sh.d_model, sh.d_ff, M, P), "ms": []}
         for m in ("ep", "llep"):
             g[m].run_ms()                      # warm-up
-        for _ in range(args.reps):             # alternate so both see the same clock / power state
+        # steady state under the power cap: each mode back to back for >= 150 ms per round, rounds
+        # alternate EP / LLEP, median over all CUDA-event-timed iterations
+        for _ in range(args.reps):
             for m in ("ep", "llep"):
-                res[m]["ms"].append(g[m].run_ms())
+                t0, n = time.perf_counter(), 0
+                while n < 3 or (time.perf_counter() - t0) * 1e3 < 150.0:
+                    res[m]["ms"].append(g[m].run_ms())
+                    n += 1
         for m in ("ep", "llep"):
-            res[m]["gemm_ms"] = statistics.median(res[m]["ms"])
+            res[m]["iters"] = len(res[m]["ms"])
+            res[m]["gemm_ms"] = statistics.median(res[m].pop("ms"))
         del g
         torch.cuda.empty_cache()
         res["gemm_speedup"] = res["ep"]["gemm_ms"] / res["llep"]["gemm_ms"]
         res["row_bound"] = res["ep"]["rows"] / res["llep"]["rows"]
+        res["modelled_layer_speedup"] = ((res["ep"]["gemm_ms"] + res["ep"]["link_ms_modelled"]) /
+                                         (res["llep"]["gemm_ms"] + res["llep"]["link_ms_modelled"]))
         print(json.dumps(res), flush=True)
         out.append(res)
     return out

@@ -16,10 +16,16 @@ UNIT = {"ns": 1, "nsecond": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 
 def short(name):
     m = re.search(r"(grouped_gemm_2cta_kernel|grouped_gemm_kernel)ILi(\d+)ELi(\d)E", name)
     if not m:
-        m = re.search(r"(grouped_gemm_2cta_kernel|grouped_gemm_kernel)<(?:\(int\))?(\d+), (?:\(int\))?(\d)>", name)
+        m = re.search(r"(grouped_gemm_2cta_kernel|grouped_gemm_kernel)<(?:\(int\))?(\d+), (?:\(int\))?(\d)[,>]", name)
     if m:
         kind = {"0": "GEMM1+SwiGLU", "1": "GEMM2+gate", "2": "GEMM1 recompute, raw gate/up (backward)"}[m.group(3)]
         return f"{m.group(1)}<{m.group(2)},{m.group(3)}> ({kind})"
+    m = re.search(r"gemm_bwd_pair_kernelILi(\d)E", name) or re.search(r"gemm_bwd_pair_kernel<(?:\(int\))?(\d)[,>]", name)
+    if m:
+        return f"gemm_bwd_pair_kernel<{m.group(1)}> ({'dY·W / dGU·W13 (MN-major B)' if m.group(1) == '0' else 'weight gradients (MN-major A, B)'})"
+    m = re.search(r"router_kernelILi(\d+)E", name) or re.search(r"router_kernel<(?:\(int\))?(\d+)", name)
+    if m:
+        return f"router_kernel<K={m.group(1)}> (Eq. 2 logits + softmax top-K)"
     m = re.search(r"gemm_bwd_kernelILi(\d)E", name) or re.search(r"gemm_bwd_kernel<(?:\(int\))?(\d)>", name)
     if m:
         return f"gemm_bwd_kernel<{m.group(1)}> ({'dY·W / dGU·W13 (MN-major B)' if m.group(1) == '0' else 'weight gradients (MN-major A, B)'})"

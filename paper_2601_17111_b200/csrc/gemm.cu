@@ -1240,7 +1240,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
   } else if (threadIdx.x == 0) {
     const int per = p.n_mt * p.n_nt;
     int pos = 0, tile = 0;
-    for (int pass = 0; pass < 2; ++pass)
+    // large (split) groups first; merging the small groups' write-bound tiles evenly among them
+    // was measured 7-10 % slower (L2 pressure on the large groups' re-read operands)
+    for (int pass = 0; pass < 2; ++pass) {
       for (int g = 0; g < p.n_groups; ++g) {
         const int ns = wgrad_splits(p.groups[g].n_rows, per, p.num_sms);
         if ((ns > 1) != (pass == 0)) continue;
@@ -1249,6 +1251,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
         ++pos;
         tile += ns * per;
       }
+    }
     s_mblk[kMaxGroups / 2 - 1] = tile;
   }
   if (warp == 0 && lane == 0) {
@@ -1524,6 +1527,10 @@ llep_status reduce_wgrad_splits(const BwdArgs &a, const int32_t *n_rows, const i
 llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s) {
   if (a.nout % 8 || a.kdim % 8 || a.mdim % 8) {
     set_error("backward GEMM needs dims %% 8 == 0");
+    return LLEP_ERR_INVALID;
+  }
+  if (a.kind == 1 && a.n_groups > kMaxGroups / 2 - 1) {   // the kernel's smem group table
+    set_error("weight-gradient GEMM supports at most %d groups per device", kMaxGroups / 2 - 1);
     return LLEP_ERR_INVALID;
   }
   BwdParams p;

@@ -395,6 +395,24 @@ def cpu_baseline(shape, hot, nhot, budget_s=12.0, max_tokens=8192):
                       f"{W.scenario_name(hot, nhot)} workload, float64 O3 (numpy BLAS), {t_total:.1f} s"}
 
 
+def metric_name(args, hot):
+    if args.config == "g120" and args.hot == 95 and args.nhot == 1:
+        return METRIC
+    return f"MoE-layer tokens/s (LLEP, {args.config}, {W.scenario_name(hot, args.nhot)})"
+
+
+def config_obj(args, shape, hot):
+    """The `config` object of the JSON line (identical for the GPU arm and the reference arm)."""
+    B, K, D, H, M = shape.tokens_per_rank, shape.top_k, shape.d_model, shape.d_ff, shape.experts_per_rank
+    return {"workload": f"{args.config}: N={shape.n_experts} experts, top-{K}, d_model={D}, d_ff={H}, "
+                        f"{B} tokens/rank, P={shape.world}, {W.scenario_name(hot, args.nhot)}; "
+                        f"lambda=1.3 alpha=1 m=1024",
+            "tokens_per_rank": B, "ep_world": shape.world, "scenario": W.scenario_name(hot, args.nhot),
+            "mem_cap_gb": args.mem_cap_gb,
+            "l2": f"inputs larger than L2 (x {B * D * 2 / 1e6:.0f} MB/rank, expert weights "
+                  f"{M * 6 * D * H / 1e9:.1f} GB/rank); no flush"}
+
+
 def gpu_main(args):
     import torch
     world, rank, local, group = dist_setup(args.gpus)
@@ -487,18 +505,11 @@ def gpu_main(args):
     step_ms = ll["ms_per_step"]
     value = world * B / (step_ms / 1e3)
     line = {
-        "metric": METRIC if args.config == "g120" and args.hot == 95 and args.nhot == 1 else
-        f"MoE-layer tokens/s (LLEP, {args.config}, {W.scenario_name(hot, args.nhot)})",
+        "metric": metric_name(args, hot),
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded counter-based generator; random-init expert weights)",
-        "config": {"workload": f"{args.config}: N={shape.n_experts} experts, top-{K}, d_model={D}, d_ff={H}, "
-                               f"{B} tokens/rank, P={world}, {W.scenario_name(hot, args.nhot)}; "
-                               f"lambda=1.3 alpha=1 m=1024",
-                   "tokens_per_rank": B, "ep_world": world, "scenario": W.scenario_name(hot, args.nhot),
-                   "mem_cap_gb": args.mem_cap_gb,
-                   "l2": f"inputs larger than L2 (x {B * D * 2 / 1e6:.0f} MB/rank, expert weights "
-                         f"{M * 6 * D * H / 1e9:.1f} GB/rank); no flush"},
+        "config": config_obj(args, shape, hot),
         "peak_gb_per_gpu": ll["peak_bytes"] / 1e9,
         "ep": ep_line,
         "speedup_vs_ep": None if ep.get("oom") else ep["ms_per_step"] / step_ms,
@@ -585,10 +596,10 @@ def reference_main(args):
     sample = (f"{per_step} tokens of rank 0 per step (all slots in experts 0..7) of the "
               f"{W.scenario_name(hot, args.nhot)} workload, float64 O3")
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "impl": "reference", "metric": metric_name(args, hot), "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"{args.config} (oracle sample)", "ep_world": world},
+        "data": "synthetic", "config": config_obj(args, shape, hot),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": int(threads), "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)

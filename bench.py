@@ -292,6 +292,30 @@ def run_router(L, shape, x, steps, warmup):
             "note": "x [B,D] bf16 read once (189 MB at G120, > L2) + W_r + ids/gates written"}
 
 
+def run_cublas_ref(shape, rows, steps):
+    """Context for the roofline: cuBLAS (torch.matmul) on ONE dense bf16 GEMM with GEMM1's FLOPs
+    ([rows, D] x [D, 2H]), timed back to back like the layer steps (same power-capped clocks).
+    Not on the product path."""
+    import torch
+    D, H = shape.d_model, shape.d_ff
+    a = torch.randn((rows, D), device="cuda", dtype=torch.bfloat16)
+    w = torch.randn((D, 2 * H), device="cuda", dtype=torch.bfloat16)
+    for _ in range(3):
+        torch.matmul(a, w)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        torch.matmul(a, w)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del a, w
+    torch.cuda.empty_cache()
+    return {"shape": f"[{rows},{D}] x [{D},{2 * H}] bf16", "ms": ms,
+            "tflops": 4.0 * rows * D * H / (ms / 1e3) / 1e12}
+
+
 def run_e2e(L, ctx, shape, host, dev, steps, warmup, world, ep=False):
     """Public API end to end: every step copies its inputs from pinned host memory (H2D), runs the
     layer (llep_prepare + llep_moe_forward) and reads the output back (D2H).  Double-buffered: the
@@ -462,6 +486,7 @@ def gpu_main(args):
         bwd_ms = run_backward(L, ll_ctx, shape, inputs, max(3, args.steps // 2), 3, world, SEED)
     ll_ctx.close()
     router = run_router(L, shape, x, max(10, args.steps), 3)
+    cublas = run_cublas_ref(shape, int(ll["my_rows"]), max(10, args.steps)) if world == 1 else None
     trace = run_trace(L, shape, rank, local, world, group, args.trace, args.steps, args.warmup) \
         if args.trace else None
 
@@ -523,6 +548,7 @@ def gpu_main(args):
                      "frac_of_sustained": achieved / peaks["bf16_tflops_sustained"],
                      "flops_per_launch": g1_flops, "ms_per_launch": g1_ms,
                      "gemm2_tflops": g2_flops / (g2_ms / 1e3) / 1e12 if g2_ms > 0 else 0.0,
+                     "cublas_dense_same_flops": cublas,
                      "layer_tflops": (g1_flops + g2_flops) / (step_ms / 1e3) / 1e12},
         "hbm": {"dispatch_gbs": (B * D * 2 + B * K * (2 * D + 4)) / (st["ms"]["dispatch"] / calls / 1e3) / 1e9
                 if world == 1 and st["ms"]["dispatch"] > 0 else None,

@@ -31,6 +31,28 @@ def worker(rank, P, cfg, pct, nhot, outdir, sample):
     x, ids, gates, w13, w2, _, _ = LC.rank_inputs(sh, rank, None if pct == 0 else pct, nhot, 21, f"cuda:{dev}")
     alpha, m, lam = (float(v) for v in os.environ.get("LLEP_TEST_PARAMS", "1,1024,1.3").split(","))
     m = int(m)
+    trace = os.environ.get("LLEP_TEST_TRACE")
+    if trace:   # row f4: replay every record of a SPEC-format trace on one context, LLEP and EP
+        recs = W.load_trace(trace, sh.n_experts, P)
+        bmax = max(int(C[p].sum()) // sh.top_k for C in recs for p in range(P))
+        ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, P, rank, dev, bmax)
+        xa = W.tokens_torch(bmax, sh.d_model, rank, f"cuda:{dev}", 21)
+        res = {}
+        for i, C in enumerate(recs):
+            ids_np = W.routing_from_counts(C[rank], sh.top_k, rank, 21 + i)
+            B = ids_np.shape[0]
+            g_np = W.gate_weights(B, sh.top_k, rank, 21 + i)
+            ids_t, g_t = torch.from_numpy(ids_np).to(f"cuda:{dev}"), torch.from_numpy(g_np).to(f"cuda:{dev}")
+            o1 = ctx(xa[:B], ids_t, g_t, w13, w2, alpha, m, lam)
+            o2 = ctx(xa[:B], ids_t, g_t, w13, w2, ep=True)
+            torch.cuda.synchronize()
+            res[f"r{i}_llep"] = o1.float().cpu().numpy()
+            res[f"r{i}_same"] = np.array(bool(torch.equal(o1, o2)))
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), n_records=np.array(len(recs)), **res)
+        dist.barrier()
+        ctx.close()
+        dist.destroy_process_group()
+        return
     ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, P, rank, dev, sh.tokens_per_rank)
     out_llep = ctx(x, ids, gates, w13, w2, alpha, m, lam)
     plan = ctx.prepare(ids, alpha, m, lam)[0]          # plan of the LLEP call (deterministic)

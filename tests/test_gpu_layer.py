@@ -277,3 +277,29 @@ def test_layer_trace_replay(L, tmp_path):
         mr, l2 = LC.errors(_to_np(out), ref)
         assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (rec, mr, l2)
     ctx.close()
+
+
+def test_multiprocess_trace_replay_p2(L, tmp_path):
+    """Row f4 at P=2 (processes sharing cuda:0): replay the six records of a SPEC-format trace whose
+    skew changes per record (tools/traces/tiny_mix_p2.csv, per-device counts) on one context per
+    rank; every record's LLEP output vs O3 on that record's routing, and LLEP == EP bitwise."""
+    trace = os.path.join(os.path.dirname(HERE), "tools", "traces", "tiny_mix_p2.csv")
+    P = 2
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29561", LLEP_TEST_TRACE=trace)
+    cmd = [sys.executable, os.path.join(HERE, "mp_layer_worker.py"), str(P), "tiny", "95", "1", str(tmp_path)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    sh0 = W.CONFIGS["tiny"]
+    recs = W.load_trace(trace, sh0.n_experts, P)
+    w = LC.OracleWeights(sh0.d_model, sh0.d_ff, 21)
+    for p in range(P):
+        res = np.load(os.path.join(tmp_path, f"rank{p}.npz"))
+        assert int(res["n_records"]) == len(recs) == 6
+        for i, C in enumerate(recs):
+            ids = W.routing_from_counts(C[p], sh0.top_k, p, 21 + i)
+            B = ids.shape[0]
+            sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, B, P)
+            ref = LC.oracle_rank_output(sh, p, ids, W.gate_weights(B, sh0.top_k, p, 21 + i), 21, weights=w)
+            mr, l2 = LC.errors(res[f"r{i}_llep"].astype(np.float64), ref)
+            assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (p, i, mr, l2)
+            assert bool(res[f"r{i}_same"])

@@ -332,6 +332,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
 // rows of the 256-row accumulator) and arrives on the leader's TMEM-empty barrier.
 // SwiGLU exchange buffer of a half tile (mode 0): [64 rows][S0+1] + [64 rows][S1+1] fp32 (odd strides)
 constexpr int kXchgBytes = 64 * (65 + 65) * 4;   // S0, S1 <= 64 for BN <= 256
+// coalesced epilogue stores: per epilogue warp a [32 rows][128 B] staging block (16-byte units
+// XOR-swizzled by row) -- mode 0 places it inside its exchange buffer
+constexpr int kStoreStageBytes = 4 * 32 * 128;
+
+// The warp's 32 lanes each hold up to 8 16-byte units of their own row (o[0..nv)); write them so
+// that one instruction stores 4 rows x 128 contiguous bytes (rows may be scattered in memory):
+// stage in shared memory, then lane l writes unit (l & 7) of row (4 i + l / 8).
+__device__ __forceinline__ void warp_store_rows(uint8_t *wst, int lane, const uint4 (&o)[8], int nv,
+                                                unsigned long long dst, int ok) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (c < nv) *reinterpret_cast<uint4 *>(wst + lane * 128 + ((c ^ (lane & 7)) * 16)) = o[c];
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int rr = it * 4 + (lane >> 3), c = lane & 7;
+    const unsigned long long d = __shfl_sync(0xffffffffu, dst, rr);
+    const int k = __shfl_sync(0xffffffffu, ok, rr);
+    if (k && c < nv)
+      *reinterpret_cast<uint4 *>(d + c * 16) = *reinterpret_cast<const uint4 *>(wst + rr * 128 + ((c ^ (rr & 7)) * 16));
+  }
+  __syncwarp();
+}
 
 template <int BN, int KSUB = 1, int XB = 0>   // KSUB: 64-deep K sub-tiles per stage; XB: exchange bytes
 struct Cfg2 {
@@ -417,7 +440,7 @@ __device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
 
 template <int BN, int MODE, int KSUB>
 __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(const __grid_constant__ GemmParams p) {
-  using C = Cfg2<BN, KSUB, MODE == 0 ? kXchgBytes : 0>;
+  using C = Cfg2<BN, KSUB, MODE == 0 ? kXchgBytes : kStoreStageBytes>;
   constexpr int KST = BK * KSUB;                 // K per pipeline stage
   constexpr int S = C::STAGES;
   constexpr int TM = 2 * BM;                     // rows per pair tile
@@ -662,67 +685,77 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
               *reinterpret_cast<uint4 *>(orow + j) = o;
             }
           }
-        }
-      } else if (MODE == 2) {
-        // raw gate / up pre-activations for the backward recompute: GU[r] = [g (nout) | u (nout)]
-        __nv_bfloat16 *grow = p.out + (size_t)row * 2 * p.nout + col0;
-#pragma unroll 1
-        for (int j = 0; j < bno; j += 8) {
-          float g[8], u[8];
-          tmem_ld8(taddr + j, g);
-          tmem_ld8(taddr + bno + j, u);
-          tmem_ld_wait();
-          if (row_ok && col0 + j < p.nout) {
-            uint4 og, ou;
-            __nv_bfloat162 *hg = reinterpret_cast<__nv_bfloat162 *>(&og);
-            __nv_bfloat162 *hu = reinterpret_cast<__nv_bfloat162 *>(&ou);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              hg[i] = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
-              hu[i] = __floats2bfloat162_rn(u[2 * i], u[2 * i + 1]);
-            }
-            *reinterpret_cast<uint4 *>(grow + j) = og;
-            *reinterpret_cast<uint4 *>(grow + p.nout + j) = ou;
-          }
-        }
-      } else if (MODE == 0) {
-        __nv_bfloat16 *orow = p.out + (size_t)row * p.nout + col0;
-#pragma unroll 1
-        for (int j = 0; j < bno; j += 8) {
-          float g[8], u[8];
-          tmem_ld8(taddr + j, g);
-          tmem_ld8(taddr + bno + j, u);
-          tmem_ld_wait();
-          if (row_ok && col0 + j < p.nout) {
-            uint4 o;
-            __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float a0 = __fdividef(g[2 * i], 1.f + __expf(-g[2 * i])) * u[2 * i];
-              const float a1 = __fdividef(g[2 * i + 1], 1.f + __expf(-g[2 * i + 1])) * u[2 * i + 1];
-              h[i] = __floats2bfloat162_rn(a0, a1);
-            }
-            *reinterpret_cast<uint4 *>(orow + j) = o;
-          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");   // exchange reads done before any reuse
         }
       } else {
-        const float gs = row_ok ? p.gate[row] : 0.f;
-        __nv_bfloat16 *orow = p.out + (size_t)row * p.nout + col0;
-        if (p.peer_slot && row_ok) {  // fused combine push: this row's output -> its home slot
-          const int32_t src = p.row_src[row];
-          orow = reinterpret_cast<__nv_bfloat16 *>(p.peer_slot[src & 31]) + (size_t)(src >> 5) * p.nout + col0;
+        // full tile: lane = row; 64-column chunks converted in registers, stored coalesced
+        uint8_t *wst = reinterpret_cast<uint8_t *>(xchg) + q * (32 * 128);
+        const int okr = row_ok ? 1 : 0;
+        float gs = 1.f;
+        __nv_bfloat16 *orow;
+        if (MODE == 1) {
+          gs = row_ok ? p.gate[row] : 0.f;
+          orow = p.out + (size_t)row * p.nout + col0;
+          if (p.peer_slot && row_ok) {  // fused combine push: this row's output -> its home slot
+            const int32_t src = p.row_src[row];
+            orow = reinterpret_cast<__nv_bfloat16 *>(p.peer_slot[src & 31]) + (size_t)(src >> 5) * p.nout + col0;
+          }
+        } else if (MODE == 0) {
+          orow = p.out + (size_t)row * p.nout + col0;
+        } else {
+          orow = p.out + (size_t)row * 2 * p.nout + col0;   // GU[r] = [g (nout) | u (nout)]
         }
 #pragma unroll 1
-        for (int j = 0; j < bno; j += 8) {
-          float v[8];
-          tmem_ld8(taddr + j, v);
-          tmem_ld_wait();
-          if (row_ok && col0 + j < p.nout) {
-            uint4 o;
-            __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+        for (int j = 0; j < bno; j += 64) {
+          const int nch = (bno - j) >= 64 ? 8 : (bno - j) / 8;
+          const int left = (p.nout - col0 - j) / 8;          // masked tail of the output width
+          const int nv = nch < left ? nch : (left > 0 ? left : 0);
+          float v[64];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(gs * v[2 * i], gs * v[2 * i + 1]);
-            *reinterpret_cast<uint4 *>(orow + j) = o;
+          for (int c = 0; c < 8; ++c)
+            if (c < nch) tmem_ld8(taddr + j + 8 * c, v + 8 * c);
+          if (MODE != 1) {
+            float u[64];
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              if (c < nch) tmem_ld8(taddr + bno + j + 8 * c, u + 8 * c);
+            tmem_ld_wait();
+            uint4 o[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o[c]);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float g0 = v[8 * c + 2 * i], g1 = v[8 * c + 2 * i + 1];
+                const float u0 = u[8 * c + 2 * i], u1 = u[8 * c + 2 * i + 1];
+                if (MODE == 0)
+                  h[i] = __floats2bfloat162_rn(__fdividef(g0, 1.f + __expf(-g0)) * u0,
+                                               __fdividef(g1, 1.f + __expf(-g1)) * u1);
+                else
+                  h[i] = __floats2bfloat162_rn(g0, g1);
+              }
+            }
+            warp_store_rows(wst, lane, o, nv, reinterpret_cast<unsigned long long>(orow + j), okr);
+            if (MODE == 2) {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o[c]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(u[8 * c + 2 * i], u[8 * c + 2 * i + 1]);
+              }
+              warp_store_rows(wst, lane, o, nv, reinterpret_cast<unsigned long long>(orow + p.nout + j), okr);
+            }
+          } else {
+            tmem_ld_wait();
+            uint4 o[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o[c]);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                h[i] = __floats2bfloat162_rn(gs * v[8 * c + 2 * i], gs * v[8 * c + 2 * i + 1]);
+            }
+            warp_store_rows(wst, lane, o, nv, reinterpret_cast<unsigned long long>(orow + j), okr);
           }
         }
       }
@@ -798,7 +831,7 @@ llep_status launch(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
 
 template <int BN, int MODE, int KSUB = 2>
 llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
-  using C = Cfg2<BN, KSUB, MODE == 0 ? kXchgBytes : 0>;
+  using C = Cfg2<BN, KSUB, MODE == 0 ? kXchgBytes : kStoreStageBytes>;
   auto kern = grouped_gemm_2cta_kernel<BN, MODE, KSUB>;
   static bool attr_set = false;
   if (!attr_set) {

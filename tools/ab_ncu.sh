@@ -3,7 +3,7 @@
 # usage: tools/ab_ncu.sh <layout> [variants] [iters]
 L=${1:-g120p1}; V=${2:-cta1,cta2}; IT=${3:-1}
 ncu --clock-control base --metrics gpu__time_duration.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum \
-    -k regex:grouped_gemm --csv python tools/gemm_bench.py --layout $L --iters $IT --variants $V 2>/dev/null \
+    -k regex:grouped_gemm --csv python tools/gemm_bench.py --layout $L --iters $IT --variants $V $GB_ARGS 2>/dev/null \
   | python -c "
 import csv,sys
 rows=[r for r in csv.reader(sys.stdin) if len(r)>10]

@@ -21,6 +21,8 @@ def layout(name):
         return [124518] + [52] * 77 + [51] * 50
     if name == "g120p8":
         return [124464] + [413] * 16
+    if name == "q3p1":          # Q3 at P=1: D=2048, H=768 (use --D 2048 --H 768)
+        return [498074] + [207] * 28 + [206] * 99
     if name == "uniform":
         return [1024] * 128
     if name.startswith("fgemm"):

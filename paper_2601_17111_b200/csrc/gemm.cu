@@ -1198,7 +1198,7 @@ constexpr int kPairB = 128 * BK * 2;       // 16 KB per CTA (half of N)
 constexpr int kPairStage = kPairA + kPairB;
 template <int KIND> struct BwdPairCfg {
   static constexpr int STAGES = KIND == 0 ? 6 : 4;
-  static constexpr int SMEM = STAGES * kPairStage + 1024 + (KIND == 1 ? kBwdNStg * kBwdStg : 0) + 1024;
+  static constexpr int SMEM = STAGES * kPairStage + 1024 + (KIND == 1 ? kBwdNStg * kBwdStg : kStoreStageBytes) + 1024;
 };
 
 template <int KIND>
@@ -1405,6 +1405,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
         const int c0 = ti.half ? (L >> 6) * (kBwdBN / 2) : 0, cw = ti.half ? kBwdBN / 2 : kBwdBN;
         const bool ok = row < ti.row_end;
         __nv_bfloat16 *orow = reinterpret_cast<__nv_bfloat16 *>(p.out) + (size_t)row * p.nout + ti.n0 + c0;
+        if (!ti.half) {   // full tile: coalesced row stores through the warp's smem stage
+          uint8_t *wst = reinterpret_cast<uint8_t *>(stg) + q * (32 * 128);
+#pragma unroll 1
+          for (int j = 0; j < kBwdBN; j += 64) {
+            const int left = (p.nout - ti.n0 - j) / 8;
+            const int nv = left < 8 ? (left > 0 ? left : 0) : 8;
+            float v[64];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) tmem_ld8(taddr + j + 8 * c, v + 8 * c);
+            tmem_ld_wait();
+            uint4 o[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o[c]);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[8 * c + 2 * i], v[8 * c + 2 * i + 1]);
+            }
+            warp_store_rows(wst, lane, o, nv, reinterpret_cast<unsigned long long>(orow + j), ok ? 1 : 0);
+          }
+        } else
 #pragma unroll 1
         for (int j = 0; j < cw; j += 8) {
           float v[8];

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(kRankThreads) local_rank_kernel(
     if (e >= N) e = -1;
     const unsigned peers = __match_any_sync(0xffffffffu, e);
     if (e >= 0 && lane == __ffs(peers) - 1) mine[e] += __popc(peers);
+    __syncwarp();   // order this round's counter updates before the next round's (other lanes)
   }
   __syncthreads();
   for (int e = threadIdx.x; e < N; e += kRankThreads) {

@@ -154,3 +154,14 @@ def test_router_validation(L):
         assert lib.llep_router(x, w, B, D, N, K, ctypes.addressof(ids), ctypes.addressof(g), None, None) == 1
         assert lib.llep_last_error()
     assert lib.llep_router(None, None, 0, 64, 8, 2, None, None, None, None) == 0
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """The binding has no CPU fallback: without the compiled library the import raises."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LLEP_LIB=str(tmp_path / "no_such_libllep.so"))
+    r = subprocess.run([sys.executable, "-c", "from paper_2601_17111_b200 import llep"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0 and ("OSError" in r.stderr or "ImportError" in r.stderr or "not found" in r.stderr), r.stderr[-500:]

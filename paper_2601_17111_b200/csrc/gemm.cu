@@ -1616,21 +1616,6 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   prm.gate = g.gate;
   prm.out = reinterpret_cast<__nv_bfloat16 *>(g.out);
   if (g.row_align == 2 * BM) {   // 2-CTA pair tiles (groups 256-row aligned)
-    if (getenv("LLEP_FWD_KSUB1")) {                   // A/B: 64-deep pipeline stages
-      if (g.mode == 0) return g.nout % 120 == 0 && g.nout % 128 ? launch_pair<240, 0, 1>(g, prm, s)
-                                                             : launch_pair<256, 0, 1>(g, prm, s);
-      if (g.mode == 1) return g.nout % 240 == 0 && g.nout % 256 ? launch_pair<240, 1, 1>(g, prm, s)
-                                                             : launch_pair<256, 1, 1>(g, prm, s);
-    }
-    if (const char *fb = getenv("LLEP_FWD_BN")) {   // A/B override of the tile width
-      const int bn = atoi(fb);
-      if (g.mode == 0 && bn == 192) return launch_pair<192, 0>(g, prm, s);
-      if (g.mode == 0 && bn == 256) return launch_pair<256, 0>(g, prm, s);
-      if (g.mode == 0 && bn == 240) return launch_pair<240, 0>(g, prm, s);
-      if (g.mode == 1 && bn == 192) return launch_pair<192, 1>(g, prm, s);
-      if (g.mode == 1 && bn == 256) return launch_pair<256, 1>(g, prm, s);
-      if (g.mode == 1 && bn == 240) return launch_pair<240, 1>(g, prm, s);
-    }
     if (g.mode == 0) {
       if (g.nout % 128 == 0) return launch_pair<256, 0>(g, prm, s);
       if (g.nout % 120 == 0) return launch_pair<240, 0>(g, prm, s);

@@ -1,12 +1,19 @@
-"""Weight-gradient GEMM (llep_gemm_bwd kind 1) on G120-P1-like group layouts, for ncu A/B.
-    python tools/wgrad_bench.py [hot|small|both] [mdim] [nout]"""
-import os, sys
+"""Weight-gradient GEMM (llep_gemm_bwd kind 1, CTA pairs) on G120-P1-like group layouts: time per
+launch (CUDA events, median of 10 after 0.4 s of back-to-back warm-up) and the output write rate.
+    python tools/wgrad_bench.py [hot|small|both] [mdim] [nout] [--1cta]"""
+import os
+import statistics
+import sys
+
 import torch
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2601_17111_b200 import llep as L
+from paper_2601_17111_b200 import llep as L  # noqa: E402
+
 which = sys.argv[1] if len(sys.argv) > 1 else "both"
 mdim = int(sys.argv[2]) if len(sys.argv) > 2 else 2880
 nout = int(sys.argv[3]) if len(sys.argv) > 3 else 2880
+pair = "--1cta" not in sys.argv
 sizes = {"hot": [124518], "small": [52] * 127, "both": [124518] + [52] * 127}[which]
 groups, rb = [], 0
 for i, n in enumerate(sizes):
@@ -18,6 +25,21 @@ for (i, r0, n) in groups:
     a[r0 + n:r0 + (n + 255) // 256 * 256] = 0
     b[r0 + n:r0 + (n + 255) // 256 * 256] = 0
 out = torch.empty(len(groups), mdim, nout, device="cuda")
-for _ in range(3):
-    L.gemm_bwd(1, a, b, groups, nout, mdim, len(groups), out=out)
-torch.cuda.synchronize()
+import time  # noqa: E402
+t0 = time.perf_counter()
+while time.perf_counter() - t0 < 0.4:          # steady state: clocks settle under the power cap
+    L.gemm_bwd(1, a, b, groups, nout, mdim, len(groups), out=out, pair=pair)
+    torch.cuda.synchronize()
+ts = []
+for _ in range(10):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    L.gemm_bwd(1, a, b, groups, nout, mdim, len(groups), out=out, pair=pair)
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+ms = statistics.median(ts)
+flops = 2.0 * mdim * nout * sum(sizes)
+wbytes = len(groups) * mdim * nout * 4
+print(f"{which} mdim={mdim} nout={nout} pair={pair}: {ms:.3f} ms, {flops / ms / 1e9:.0f} TFLOP/s, "
+      f"output {wbytes / 1e9:.2f} GB -> {wbytes / ms / 1e6:.0f} GB/s", flush=True)

@@ -518,9 +518,10 @@ def gpu_main(args):
     g1_flops = 4.0 * D * H * rows_per_launch
     g2_flops = 2.0 * D * H * rows_per_launch
     achieved = g1_flops / (g1_ms / 1e3) / 1e12 if g1_ms > 0 else 0.0
-    # the GEMMs run inside ~5-10 ms steps at near-max SM clock (see "clocks"), so the burst figure is
-    # the denominator; the sustained (seconds-long, power-capped) fraction is reported beside it
-    peak = peaks["bf16_tflops"]
+    # the GEMM is timed inside a long loop of layer steps (hundreds of ms back to back, the SM clock
+    # settles under the power cap -- see "clocks"), so the contract's denominator is the SUSTAINED
+    # measured bf16 figure; the burst one is reported beside it
+    peak = peaks["bf16_tflops_sustained"]
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -544,8 +545,8 @@ def gpu_main(args):
         "phases_ms_per_step": {k: v / calls for k, v in st["ms"].items()},
         "roofline": {"kernel": "grouped GEMM1 + SwiGLU (tcgen05)", "bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                     "peak_kind": f"bf16 dense, burst, {peaks['source']}",
-                     "frac_of_sustained": achieved / peaks["bf16_tflops_sustained"],
+                     "peak_kind": f"bf16 dense, sustained (kernel timed inside a long step loop), {peaks['source']}",
+                     "frac_of_burst": achieved / peaks["bf16_tflops"],
                      "flops_per_launch": g1_flops, "ms_per_launch": g1_ms,
                      "gemm2_tflops": g2_flops / (g2_ms / 1e3) / 1e12 if g2_ms > 0 else 0.0,
                      "cublas_dense_same_flops": cublas,

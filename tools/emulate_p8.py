@@ -122,14 +122,18 @@ def main():
                          "link_ms_modelled": 1e3 * link_seconds(plan, cnt, sh.d_model, sh.d_ff, M, P), "ms": []}
         for m in ("ep", "llep"):
             g[m].run_ms()                      # warm-up
-        # steady state under the power cap: each mode back to back for >= 150 ms per round, rounds
-        # alternate EP / LLEP, median over all CUDA-event-timed iterations
+        # steady state under the power cap: 0.3 s of back-to-back warm-up, then EP and LLEP iterations
+        # strictly alternating for >= 0.3 s per rep (both arms see the same clock / thermal state),
+        # median over all CUDA-event-timed iterations
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < 0.3:
+            g["llep"].run_ms()
         for _ in range(args.reps):
-            for m in ("ep", "llep"):
-                t0, n = time.perf_counter(), 0
-                while n < 3 or (time.perf_counter() - t0) * 1e3 < 150.0:
+            t0, n = time.perf_counter(), 0
+            while n < 3 or time.perf_counter() - t0 < 0.3:
+                for m in ("ep", "llep"):
                     res[m]["ms"].append(g[m].run_ms())
-                    n += 1
+                n += 1
         for m in ("ep", "llep"):
             res[m]["iters"] = len(res[m]["ms"])
             res[m]["gemm_ms"] = statistics.median(res[m].pop("ms"))

@@ -245,20 +245,34 @@ def run_backward(L, ctx, shape, inputs, steps, warmup, world, seed):
     dw13 = torch.empty((M, 2 * H, D), dtype=torch.float32, device=x.device)
     dw2 = torch.empty((M, D, H), dtype=torch.float32, device=x.device)
 
+    out = torch.empty_like(x)
+    gu = [None]
+
     def step():
         plan, _ = ctx.prepare(ids, plan_out=plan_buf)
         ctx.backward(x, ids, gates, dout, w13, w2, plan, dx, dg, dw13, dw2)
 
-    for _ in range(warmup):
-        step()
-    barrier(world)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        step()
-    e1.record()
-    barrier(world)
-    return max_over_ranks(e0.elapsed_time(e1), world) / steps
+    def train_step():
+        # training step on saved pre-activations: prepare + llep_moe_forward_train + llep_moe_backward_saved
+        plan, req = ctx.prepare(ids, plan_out=plan_buf)
+        if gu[0] is None or gu[0].shape[0] < req.rows_needed:
+            gu[0] = torch.empty((int(req.rows_needed), 2 * H), dtype=torch.bfloat16, device=x.device)
+        ctx.forward_train(x, ids, gates, w13, w2, plan, out, gu[0])
+        ctx.backward(x, ids, gates, dout, w13, w2, plan, dx, dg, dw13, dw2, gu=gu[0])
+
+    res = []
+    for fn in (step, train_step):
+        for _ in range(warmup):
+            fn()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        barrier(world)
+        res.append(max_over_ranks(e0.elapsed_time(e1), world) / steps)
+    return res
 
 
 def run_router(L, shape, x, steps, warmup):
@@ -483,7 +497,7 @@ def gpu_main(args):
                        "double-buffered on copy streams"}
     bwd_ms = None
     if not args.no_backward:
-        bwd_ms = run_backward(L, ll_ctx, shape, inputs, max(3, args.steps // 2), 3, world, SEED)
+        bwd_ms, train_ms = run_backward(L, ll_ctx, shape, inputs, max(3, args.steps // 2), 3, world, SEED)
     ll_ctx.close()
     router = run_router(L, shape, x, max(10, args.steps), 3)
     cublas = run_cublas_ref(shape, int(ll["my_rows"]), max(10, args.steps)) if world == 1 else None
@@ -565,7 +579,12 @@ def gpu_main(args):
                             "fwd_bwd_tokens_s": world * B / ((bwd_ms + step_ms) / 1e3),
                             "tflops": bwd_flops / (bwd_ms / 1e3) / 1e12,
                             "note": "llep_prepare + llep_moe_backward (recomputes the forward internals; "
-                                    "dx, dgates, dW13, dW_down incl. spilled-expert gradient return)"}
+                                    "dx, dgates, dW13, dW_down incl. spilled-expert gradient return)",
+                            "train_step": {"ms_per_step": train_ms, "tokens_s": world * B / (train_ms / 1e3),
+                                           "tflops": 18.0 * D * H * rows_per_launch / (train_ms / 1e3) / 1e12,
+                                           "note": "llep_prepare + llep_moe_forward_train (saves [g|u]) + "
+                                                   "llep_moe_backward_saved (no GU recompute): one training step "
+                                                   "of the layer; tflops over 18·D·H per routed row"}}
     router["frac_hbm"] = router["gbs"] / peaks["hbm_gbs"]
     line["router"] = router
     if trace:

@@ -208,6 +208,19 @@ llep_status llep_moe_forward(llep_context *ctx, const uint16_t *x, const int32_t
                              const float *topk_w, int64_t n_tokens, const uint16_t *w13,
                              const uint16_t *w2, const void *plan, uint16_t *out, void *stream);
 
+/* llep_moe_forward_train -- llep_moe_forward for a training step (row f1): identical outputs,
+ * and GEMM1's epilogue also stores this rank's raw gate / up pre-activations
+ *   gu_save [gu_rows, 2H] bf16, device, caller-owned: row r of this rank's receive layout holds
+ *           [X_r W_gateᵀ | X_r W_upᵀ] (bf16 of the fp32 tensor-core accumulator; padding rows of a
+ *           group are left untouched).  gu_rows >= this rank's padded layout rows, which
+ *           llep_requirements.rows_needed of the same llep_prepare always covers.
+ * Pass the buffer and the same plan to llep_moe_backward_saved, which then skips recomputing
+ * X·W13ᵀ.  Errors: as llep_moe_forward; INVALID if gu_save is NULL or gu_rows is too small. */
+llep_status llep_moe_forward_train(llep_context *ctx, const uint16_t *x, const int32_t *topk_ids,
+                                   const float *topk_w, int64_t n_tokens, const uint16_t *w13,
+                                   const uint16_t *w2, const void *plan, uint16_t *out, uint16_t *gu_save,
+                                   int64_t gu_rows, void *stream);
+
 /* llep_moe_backward -- the backward pass of the layer (row f1) under the plan of
  * llep_prepare for these topk_ids, recomputing the forward internals (nothing is kept from a
  * forward call), for the loss L with dL/dout = dout:
@@ -225,6 +238,17 @@ llep_status llep_moe_backward(llep_context *ctx, const uint16_t *x, const int32_
                               const float *topk_w, const uint16_t *dout, int64_t n_tokens,
                               const uint16_t *w13, const uint16_t *w2, const void *plan, uint16_t *dx,
                               float *dgates, float *dw13, float *dw2, void *stream);
+
+/* llep_moe_backward_saved -- llep_moe_backward with the pre-activations saved by
+ * llep_moe_forward_train under the SAME plan (gu_saved [gu_rows, 2H] bf16, device, read only): the
+ * GU = X·W13ᵀ recompute is skipped; every output is bit-identical to llep_moe_backward's (the saved
+ * values come from the same kernel with the same K order).  Errors: as llep_moe_backward; INVALID if
+ * gu_saved is NULL or gu_rows is smaller than this rank's padded layout rows. */
+llep_status llep_moe_backward_saved(llep_context *ctx, const uint16_t *x, const int32_t *topk_ids,
+                                    const float *topk_w, const uint16_t *dout, int64_t n_tokens,
+                                    const uint16_t *w13, const uint16_t *w2, const void *plan,
+                                    const uint16_t *gu_saved, int64_t gu_rows, uint16_t *dx, float *dgates,
+                                    float *dw13, float *dw2, void *stream);
 
 /* ------------------------------------------------------------------ measurement
  * Per-phase device time, from CUDA events recorded on the caller's stream at the phase

@@ -783,9 +783,10 @@ static llep_status push_weights(llep_context *c, const uint16_t *w13, const uint
   return LLEP_OK;
 }
 
-llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *ids,
-                             const float *topk_w, int64_t B, const uint16_t *w13,
-                             const uint16_t *w2, const void *plan, uint16_t *out, void *stream) {
+static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t *ids,
+                               const float *topk_w, int64_t B, const uint16_t *w13,
+                               const uint16_t *w2, const void *plan, uint16_t *out, uint16_t *gu_save,
+                               int64_t gu_rows, void *stream) {
   if (!c || !plan || !w13 || !w2 || (B > 0 && (!x || !ids || !topk_w || !out)))
     return invalid("null pointer");
   if (B != c->prepared_tokens) return invalid("n_tokens differs from the last llep_prepare");
@@ -804,6 +805,11 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   }
   const int N = c->N, P = c->P, M = c->M, D = c->D, H = c->H;
   (void)H;
+  if (gu_save && gu_rows < sum.my_padded) {
+    set_error("gu_save holds %lld rows, this rank's layout needs %lld (llep_requirements.rows_needed "
+              "is always enough)", (long long)gu_rows, (long long)sum.my_padded);
+    return LLEP_ERR_INVALID;
+  }
   // a7: weight migration, pushed by the native device on a side stream (copy engines); row f2: each
   // destination's GEMM waits for a foreign slot's flag only when it reaches that slot's tiles
   bool any_copy = false;
@@ -840,7 +846,8 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   uint16_t *X = reinterpret_cast<uint16_t *>(c->arena + c->off_x);
   GemmArgs g1;
   memset(&g1, 0, sizeof(g1));
-  g1.mode = 0;
+  g1.mode = gu_save ? 3 : 0;   // training forward: also save the raw [g | u] for the backward
+  g1.out2 = gu_save;
   g1.a = X;
   g1.a_rows = c->arena_rows;
   g1.kdim = D;
@@ -867,6 +874,7 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
   // a9: GEMM2 + gate   A [rows, H] -> Y [rows, D]  (Y reuses X's rows: X is dead after GEMM1)
   GemmArgs g2 = g1;
   g2.mode = 1;
+  g2.out2 = nullptr;
   g2.a = c->act;
   g2.kdim = H;
   g2.w_native = w2;
@@ -896,6 +904,20 @@ llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *
 }
 
 
+llep_status llep_moe_forward(llep_context *c, const uint16_t *x, const int32_t *ids, const float *topk_w,
+                             int64_t B, const uint16_t *w13, const uint16_t *w2, const void *plan,
+                             uint16_t *out, void *stream) {
+  return moe_forward(c, x, ids, topk_w, B, w13, w2, plan, out, nullptr, 0, stream);
+}
+
+llep_status llep_moe_forward_train(llep_context *c, const uint16_t *x, const int32_t *ids,
+                                   const float *topk_w, int64_t B, const uint16_t *w13, const uint16_t *w2,
+                                   const void *plan, uint16_t *out, uint16_t *gu_save, int64_t gu_rows,
+                                   void *stream) {
+  if (!gu_save) return invalid("null pointer (gu_save)");
+  return moe_forward(c, x, ids, topk_w, B, w13, w2, plan, out, gu_save, gu_rows, stream);
+}
+
 // This rank's expert groups in the layout kernel's order (native with rows, then foreign, ascending
 // ids), from the host copy of the plan: rows, weight slot (>= 0 native, -1-f foreign), expert.
 static void my_groups_host(const llep_context *c, std::vector<int32_t> &rows, std::vector<int32_t> &wslot,
@@ -924,10 +946,11 @@ static void my_groups_host(const llep_context *c, std::vector<int32_t> &rows, st
     }
 }
 
-llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t *ids,
-                              const float *topk_w, const uint16_t *dout, int64_t B,
-                              const uint16_t *w13, const uint16_t *w2, const void *plan, uint16_t *dx,
-                              float *dgates, float *dw13, float *dw2, void *stream) {
+static llep_status moe_backward(llep_context *c, const uint16_t *x, const int32_t *ids,
+                                const float *topk_w, const uint16_t *dout, int64_t B,
+                                const uint16_t *w13, const uint16_t *w2, const void *plan, uint16_t *dx,
+                                float *dgates, float *dw13, float *dw2, const uint16_t *gu_saved,
+                                int64_t gu_rows, void *stream) {
   if (!c || !plan || !w13 || !w2 || !dw13 || !dw2 ||
       (B > 0 && (!x || !ids || !topk_w || !dout || !dx || !dgates)))
     return invalid("null pointer");
@@ -946,6 +969,11 @@ llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t 
               "llep_context_reserve", (long long)sum.rows_needed, sum.foreign_needed, gslots,
               (long long)c->arena_rows, c->arena_foreign, c->arena_grad);
     return LLEP_ERR_PLAN;
+  }
+  if (gu_saved && gu_rows < sum.my_padded) {
+    set_error("gu_saved holds %lld rows, this rank's layout needs %lld", (long long)gu_rows,
+              (long long)sum.my_padded);
+    return LLEP_ERR_INVALID;
   }
   const int N = c->N, P = c->P, M = c->M, D = c->D, H = c->H;
   const PlanLayout L = plan_layout(N, P);
@@ -998,7 +1026,9 @@ llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t 
   if (G_ > 0) {
     LLEP_CUDA(launch_zero_pad(c->groups, G_, D, X, O, s));
     ++c->launches;
-    // GU = X · W13ᵀ (raw gate / up pre-activations)
+    // GU = X · W13ᵀ (raw gate / up pre-activations): recomputed, unless the training forward saved
+    // them under this plan (bit-identical: same kernel, same K order)
+    const uint16_t *GU = gu_saved ? gu_saved : c->gu;
     GemmArgs g1;
     memset(&g1, 0, sizeof(g1));
     g1.mode = 2;
@@ -1016,8 +1046,10 @@ llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t 
     g1.out = c->gu;
     g1.num_sms = c->num_sms;
     g1.row_align = c->row_align;
-    if ((st = run_grouped_gemm(g1, s)) != LLEP_OK) return st;
-    ++c->launches;
+    if (!gu_saved) {
+      if ((st = run_grouped_gemm(g1, s)) != LLEP_OK) return st;
+      ++c->launches;
+    }
     // dA0 = dO · W_down  (W_down [D][H] row-major: MN-major B)
     BwdArgs b;
     memset(&b, 0, sizeof(b));
@@ -1040,7 +1072,7 @@ llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t 
     if ((st = run_gemm_bwd(b, s)) != LLEP_OK) return st;
     ++c->launches;
     // SwiGLU backward per row; dL/dw replaces the gate in G
-    LLEP_CUDA(launch_bwd_swiglu(c->groups, G_, (int)sum.my_padded, H, c->gu, c->da0, G, c->aw, c->dgu, s));
+    LLEP_CUDA(launch_bwd_swiglu(c->groups, G_, (int)sum.my_padded, H, GU, c->da0, G, c->aw, c->dgu, s));
     ++c->launches;
     // dW_down = dOᵀ · (w a)   and   dW13 = [dg|du]ᵀ · X   (native -> dw2/dw13, foreign -> staging);
     // large groups are split along their rows, partials summed in fixed order (deterministic)
@@ -1160,6 +1192,23 @@ llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t 
     }
   }
   return LLEP_OK;
+}
+
+llep_status llep_moe_backward(llep_context *c, const uint16_t *x, const int32_t *ids, const float *topk_w,
+                              const uint16_t *dout, int64_t B, const uint16_t *w13, const uint16_t *w2,
+                              const void *plan, uint16_t *dx, float *dgates, float *dw13, float *dw2,
+                              void *stream) {
+  return moe_backward(c, x, ids, topk_w, dout, B, w13, w2, plan, dx, dgates, dw13, dw2, nullptr, 0, stream);
+}
+
+llep_status llep_moe_backward_saved(llep_context *c, const uint16_t *x, const int32_t *ids,
+                                    const float *topk_w, const uint16_t *dout, int64_t B, const uint16_t *w13,
+                                    const uint16_t *w2, const void *plan, const uint16_t *gu_saved,
+                                    int64_t gu_rows, uint16_t *dx, float *dgates, float *dw13, float *dw2,
+                                    void *stream) {
+  if (!gu_saved) return invalid("null pointer (gu_saved)");
+  return moe_backward(c, x, ids, topk_w, dout, B, w13, w2, plan, dx, dgates, dw13, dw2, gu_saved, gu_rows,
+                      stream);
 }
 
 llep_status llep_context_set_timing(llep_context *c, int32_t enable) {

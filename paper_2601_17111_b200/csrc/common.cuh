@@ -200,6 +200,7 @@ struct GemmArgs {
   int32_t n_groups_host;
   const float *gate;         // [rows] (mode 1)
   uint16_t *out;             // [rows, nout]
+  uint16_t *out2;            // mode 3 (GEMM1 + SwiGLU that also saves [g | u]): [rows, 2*nout]
   const uint32_t *wflags;    // row f2: foreign slot f's weights landed when wflags[f] >= wepoch
   uint32_t wepoch;           //         (nullptr: weights already resident)
   const int32_t *row_src;    // mode 1 push epilogue: (slot << 5) | rank of each receive row, and

@@ -48,6 +48,7 @@ struct GemmParams {
   uint32_t wepoch;
   const int32_t *row_src;
   uint16_t *const *peer_slot;
+  __nv_bfloat16 *out2;   // mode 3: raw [g | u] pre-activations, rows of 2 * nout (training forward)
 };
 
 // Row f2: wait until foreign slot f's weights have landed (flag published by the native device
@@ -371,7 +372,7 @@ struct Cfg2 {
 
 template <int BN, int MODE, int KSUB>
 __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(const __grid_constant__ GemmParams p) {
-  using C = Cfg2<BN, KSUB, MODE == 0 ? kXchgBytes : kStoreStageBytes>;
+  using C = Cfg2<BN, KSUB, (MODE == 0 || MODE == 3) ? kXchgBytes : kStoreStageBytes>;
   constexpr int KST = BK * KSUB;                 // K per pipeline stage
   constexpr int S = C::STAGES;
   constexpr int TM = 2 * BM;                     // rows per pair tile
@@ -569,6 +570,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
           // SwiGLU needs g (lanes 0-63) and u (lanes 64-127) of the same row: exchange through
           // shared memory.  Gate lanes finish columns [0, S0), up lanes [S0, BH).
           constexpr int S0 = (BH / 2 + 7) / 8 * 8, S1 = BH - S0;
+          if (MODE == 3) {   // saved pre-activations: gate lanes write g, up lanes u (as mode 2)
+            __nv_bfloat16 *dst = p.out2 + (size_t)hrow * 2 * p.nout + hi * p.nout + col0;
+#pragma unroll 1
+            for (int j = 0; j < BH; j += 8) {
+              float v[8];
+              tmem_ld8(taddr + j, v);
+              tmem_ld_wait();
+              if (hok && col0 + j < p.nout) {
+                uint4 o;
+                __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+                *reinterpret_cast<uint4 *>(dst + j) = o;
+              }
+            }
+          }
           float *xu = xchg;                          // [64][S0+1] up values of columns [0, S0)
           float *xg = xchg + 64 * (S0 + 1);          // [64][S1+1] gate values of columns [S0, BH)
           asm volatile("bar.sync 1, 128;" ::: "memory");   // the previous half tile's reads are done
@@ -631,7 +648,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
             const int32_t src = p.row_src[row];
             orow = reinterpret_cast<__nv_bfloat16 *>(p.peer_slot[src & 31]) + (size_t)(src >> 5) * p.nout + col0;
           }
-        } else if (MODE == 0) {
+        } else if (MODE == 0 || MODE == 3) {
           orow = p.out + (size_t)row * p.nout + col0;
         } else {
           orow = p.out + (size_t)row * 2 * p.nout + col0;   // GU[r] = [g (nout) | u (nout)]
@@ -659,7 +676,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
               for (int i = 0; i < 4; ++i) {
                 const float g0 = v[8 * c + 2 * i], g1 = v[8 * c + 2 * i + 1];
                 const float u0 = u[8 * c + 2 * i], u1 = u[8 * c + 2 * i + 1];
-                if (MODE == 0)
+                if (MODE != 2)
                   h[i] = __floats2bfloat162_rn(__fdividef(g0, 1.f + __expf(-g0)) * u0,
                                                __fdividef(g1, 1.f + __expf(-g1)) * u1);
                 else
@@ -667,6 +684,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
               }
             }
             warp_store_rows(wst, lane, o, nv, reinterpret_cast<unsigned long long>(orow + j), okr);
+            if (MODE == 3) {   // saved pre-activations [g | u] of this row (bit-identical to mode 2)
+              __nv_bfloat16 *grow = p.out2 + (size_t)row * 2 * p.nout + col0;
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o[c]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[8 * c + 2 * i], v[8 * c + 2 * i + 1]);
+              }
+              warp_store_rows(wst, lane, o, nv, reinterpret_cast<unsigned long long>(grow + j), okr);
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o[c]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(u[8 * c + 2 * i], u[8 * c + 2 * i + 1]);
+              }
+              warp_store_rows(wst, lane, o, nv, reinterpret_cast<unsigned long long>(grow + p.nout + j), okr);
+            }
             if (MODE == 2) {
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
@@ -762,7 +796,7 @@ llep_status launch(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
 
 template <int BN, int MODE, int KSUB = 2>
 llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
-  using C = Cfg2<BN, KSUB, MODE == 0 ? kXchgBytes : kStoreStageBytes>;
+  using C = Cfg2<BN, KSUB, (MODE == 0 || MODE == 3) ? kXchgBytes : kStoreStageBytes>;
   auto kern = grouped_gemm_2cta_kernel<BN, MODE, KSUB>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1615,7 +1649,18 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   prm.nout = g.nout;
   prm.gate = g.gate;
   prm.out = reinterpret_cast<__nv_bfloat16 *>(g.out);
+  prm.out2 = reinterpret_cast<__nv_bfloat16 *>(g.out2);
+  if (g.mode == 3 && !g.out2) {
+    set_error("grouped GEMM mode 3 needs the pre-activation output");
+    return LLEP_ERR_INVALID;
+  }
   if (g.row_align == 2 * BM) {   // 2-CTA pair tiles (groups 256-row aligned)
+    if (g.mode == 3) {
+      if (g.nout % 128 == 0) return launch_pair<256, 3>(g, prm, s);
+      if (g.nout % 120 == 0) return launch_pair<240, 3>(g, prm, s);
+      if (g.nout % 96 == 0) return launch_pair<192, 3>(g, prm, s);
+      return launch_pair<256, 3>(g, prm, s);
+    }
     if (g.mode == 0) {
       if (g.nout % 128 == 0) return launch_pair<256, 0>(g, prm, s);
       if (g.nout % 120 == 0) return launch_pair<240, 0>(g, prm, s);
@@ -1632,6 +1677,16 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
     if (g.nout % 240 == 0) return launch_pair<240, 1>(g, prm, s);
     if (g.nout % 192 == 0) return launch_pair<192, 1>(g, prm, s);
     return launch_pair<256, 1>(g, prm, s);
+  }
+  if (g.mode == 3) {   // 1-CTA tiles: SwiGLU output, then the raw pre-activations (same MMAs)
+    GemmArgs g0 = g;
+    g0.mode = 0;
+    llep_status st = run_grouped_gemm(g0, s);
+    if (st != LLEP_OK) return st;
+    g0.mode = 2;
+    g0.out = g.out2;
+    g0.out2 = nullptr;
+    return run_grouped_gemm(g0, s);
   }
   // tile width: widest instantiated N that divides the output (else masked tail tiles)
   if (g.mode == 0) {

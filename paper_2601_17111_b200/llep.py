@@ -75,6 +75,9 @@ _SIGS = {
     "llep_prepare": (ctypes.c_int, [_vp, _vp, _i64, ctypes.POINTER(Params), _i32, _vp,
                                     ctypes.POINTER(Requirements), _vp]),
     "llep_moe_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "llep_moe_forward_train": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
+    "llep_moe_backward_saved": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp,
+                                               _vp, _vp, _vp]),
     "llep_debug_copy": (ctypes.c_int, [_vp, _i32, _vp, _i64, _vp]),
     "llep_context_set_timing": (ctypes.c_int, [_vp, _i32]),
     "llep_context_stats": (ctypes.c_int, [_vp, ctypes.c_void_p, _i32]),
@@ -275,7 +278,28 @@ class Context:
                                      _stream_ptr()))
         return out
 
-    def backward(self, x, topk_ids, topk_w, dout, w13, w2, plan, dx=None, dgates=None, dw13=None, dw2=None):
+    def forward_train(self, x, topk_ids, topk_w, w13, w2, plan, out=None, gu=None):
+        """llep_moe_forward_train: forward + this rank's raw [g | u] pre-activations saved for
+        backward(..., gu=...).  Returns (out, gu); gu [rows_needed, 2H] bf16 unless given."""
+        import torch
+        B = x.shape[0]
+        for t, dt in ((x, torch.bfloat16), (topk_ids, torch.int32), (topk_w, torch.float32),
+                      (w13, torch.bfloat16), (w2, torch.bfloat16)):
+            assert t.dtype == dt and t.is_cuda and t.is_contiguous(), (t.dtype, dt)
+        assert w13.shape == (self.M, 2 * self.H, self.D) and w2.shape == (self.M, self.D, self.H)
+        if out is None:
+            out = torch.empty((B, self.D), dtype=torch.bfloat16, device=x.device)
+        if gu is None:
+            rows = int(self.last_req.rows_needed) if self.last_req is not None else 0
+            gu = torch.empty((max(rows, 1), 2 * self.H), dtype=torch.bfloat16, device=x.device)
+        assert gu.dtype == torch.bfloat16 and gu.is_contiguous() and gu.shape[1] == 2 * self.H
+        _check(_lib.llep_moe_forward_train(self._h, x.data_ptr(), topk_ids.data_ptr(), topk_w.data_ptr(), B,
+                                           w13.data_ptr(), w2.data_ptr(), plan.data_ptr(), out.data_ptr(),
+                                           gu.data_ptr(), gu.shape[0], _stream_ptr()))
+        return out, gu
+
+    def backward(self, x, topk_ids, topk_w, dout, w13, w2, plan, dx=None, dgates=None, dw13=None, dw2=None,
+                 gu=None):
         """llep_moe_backward under `plan` (from prepare on these topk_ids): returns
         (dx [B, D] bf16, dgates [B, K] fp32, dw13 [M, 2H, D] fp32, dw2 [M, D, H] fp32)."""
         import torch
@@ -286,6 +310,13 @@ class Context:
         dgates = torch.empty((B, self.K), dtype=torch.float32, device=dev) if dgates is None else dgates
         dw13 = torch.empty((self.M, 2 * self.H, self.D), dtype=torch.float32, device=dev) if dw13 is None else dw13
         dw2 = torch.empty((self.M, self.D, self.H), dtype=torch.float32, device=dev) if dw2 is None else dw2
+        if gu is not None:   # pre-activations saved by forward_train under the same plan
+            assert gu.dtype == torch.bfloat16 and gu.is_contiguous() and gu.shape[1] == 2 * self.H
+            _check(_lib.llep_moe_backward_saved(self._h, x.data_ptr(), topk_ids.data_ptr(), topk_w.data_ptr(),
+                                                dout.data_ptr(), B, w13.data_ptr(), w2.data_ptr(), plan.data_ptr(),
+                                                gu.data_ptr(), gu.shape[0], dx.data_ptr(), dgates.data_ptr(),
+                                                dw13.data_ptr(), dw2.data_ptr(), _stream_ptr()))
+            return dx, dgates, dw13, dw2
         _check(_lib.llep_moe_backward(self._h, x.data_ptr(), topk_ids.data_ptr(), topk_w.data_ptr(),
                                       dout.data_ptr(), B, w13.data_ptr(), w2.data_ptr(), plan.data_ptr(),
                                       dx.data_ptr(), dgates.data_ptr(), dw13.data_ptr(), dw2.data_ptr(),

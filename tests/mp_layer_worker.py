@@ -69,6 +69,12 @@ def worker(rank, P, cfg, pct, nhot, outdir, sample):
         plan_b, _ = ctx.prepare(ids, alpha, m, lam)
         dx, dg, dw13, dw2 = ctx.backward(x, ids, gates, dout, w13, w2, plan_b)
         torch.cuda.synchronize()
+        # training path: forward that saves [g | u], backward from the saved values == recompute
+        _, gu = ctx.forward_train(x, ids, gates, w13, w2, plan_b)
+        saved = ctx.backward(x, ids, gates, dout, w13, w2, plan_b, gu=gu)
+        torch.cuda.synchronize()
+        for a_, b_ in zip(saved, (dx, dg, dw13, dw2)):
+            assert torch.equal(a_, b_), "saved-preactivation backward differs from the recompute"
         extra = dict(dx=dx[:n].float().cpu().numpy(), dgates=dg[:n].cpu().numpy(), dw13=dw13.cpu().numpy(),
                      dw2=dw2.cpu().numpy())
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), llep=out_llep[:n].float().cpu().numpy(),

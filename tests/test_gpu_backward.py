@@ -147,3 +147,50 @@ def test_backward_multiprocess(L, tmp_path, P, pct, nhot, params):
     for p in range(P):
         got = (res[p]["dx"], res[p]["dgates"], res[p]["dw13"], res[p]["dw2"])
         _check_grads(sh, got, dx[p], dg[p], dW, range(p * M, (p + 1) * M), p * M)
+
+
+@pytest.mark.parametrize("cfg", [
+    ("tiny", 95, 1),                       # H=512: BN=256 tiles
+    ((16, 4, 512, 360, 6000), 95, 1),      # H=360: BN=240 tiles, ragged groups, half tiles
+    ((16, 4, 512, 360, 6000), None, 0),    # balanced
+])
+def test_training_forward_saved_preactivations(L, cfg):
+    """llep_moe_forward_train returns the forward's output bit for bit and saves [g | u]; the
+    backward from the saved pre-activations (llep_moe_backward_saved) equals the recomputing
+    llep_moe_backward bit for bit, and the saved rows equal X·W13ᵀ (fp32 torch) to bf16 rounding."""
+    name, pct, nhot = cfg
+    if isinstance(name, str):
+        base = W.CONFIGS[name]
+        sh = W.LayerShape(base.n_experts, base.top_k, base.d_model, base.d_ff, base.tokens_per_rank, 1)
+    else:
+        sh = W.LayerShape(*name, 1)
+    seed = 29
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, pct, nhot, seed, "cuda")
+    dout = torch.from_numpy(_dout(sh, 0, seed).view(np.int16)).cuda().view(torch.bfloat16)
+    ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, 1, 0, 0, sh.tokens_per_rank)
+    ctx.enable_backward()
+    plan, req = ctx.prepare(ids)
+    out_ref = ctx.forward(x, ids, gates, w13, w2, plan)
+    out, gu = ctx.forward_train(x, ids, gates, w13, w2, plan)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out_ref)
+    ref = ctx.backward(x, ids, gates, dout, w13, w2, plan)
+    got = ctx.backward(x, ids, gates, dout, w13, w2, plan, gu=gu)
+    torch.cuda.synchronize()
+    for a, b, n in zip(got, ref, ("dx", "dgates", "dw13", "dw2")):
+        assert torch.equal(a, b), n
+    # saved rows of every group vs fp32 torch: at P=1 row i of expert e's group is the token of e's
+    # i-th slot in flat order t·K+k (R11)
+    groups = ctx.debug(L.DBG_GROUPS, req.my_groups * 8, torch.int32).view(-1, 8).cpu().numpy()
+    flat = ids_np.reshape(-1)
+    for grp in groups:
+        e, rb, n = int(grp[0]), int(grp[2]), int(grp[3])
+        tok = torch.from_numpy(np.nonzero(flat == e)[0][:64] // sh.top_k).cuda()
+        assert n == int((flat == e).sum())
+        want = x[tok].float() @ w13[e].float().t()
+        have = gu[rb:rb + len(tok)].float()
+        assert (have - want).abs().max().item() <= 1e-2 * want.abs().max().item() + 1e-6, e
+    with pytest.raises(L.LLEPError) as ei:
+        ctx.forward_train(x, ids, gates, w13, w2, plan, gu=gu[:1])
+    assert ei.value.code == 1
+    ctx.close()

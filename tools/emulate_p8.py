@@ -109,7 +109,7 @@ def main():
         hot = None if pct == 0 else pct
         cnt = W.slot_counts(sh.n_experts, sh.tokens_per_rank * sh.top_k, hot, nhot)
         loads = (cnt * P).tolist()   # every rank draws the same per-expert slot counts (exact multiset)
-        res = {"scenario": W.scenario_name(hot, nhot)}
+        res = {"config": args.config, "world": P, "scenario": W.scenario_name(hot, nhot)}
         g = {}
         for mode in ("ep", "llep"):
             plan = L.plan_host(loads, P, 1.0, 1024, 1.3, ep=(mode == "ep"))

@@ -23,6 +23,12 @@ def layout(name):
         return [124464] + [413] * 16
     if name == "q3p1":          # Q3 at P=1: D=2048, H=768 (use --D 2048 --H 768)
         return [498074] + [207] * 28 + [206] * 99
+    if name == "dense":         # one group with G120-P1's real rows (no cold experts)
+        return [131072]
+    if name == "hot":           # G120-P1's hot group alone
+        return [124518]
+    if name == "cold":          # G120-P1's 127 cold groups alone
+        return [52] * 77 + [51] * 50
     if name == "uniform":
         return [1024] * 128
     if name.startswith("fgemm"):

@@ -18,7 +18,7 @@ def short(name):
     if not m:
         m = re.search(r"(grouped_gemm_2cta_kernel|grouped_gemm_kernel)<(?:\(int\))?(\d+), (?:\(int\))?(\d)[,>]", name)
     if m:
-        kind = {"0": "GEMM1+SwiGLU", "1": "GEMM2+gate", "2": "GEMM1 recompute, raw gate/up (backward)"}[m.group(3)]
+        kind = {"0": "GEMM1+SwiGLU", "1": "GEMM2+gate", "2": "GEMM1 recompute, raw gate/up (backward)", "3": "GEMM1+SwiGLU saving [g|u] (training forward)"}[m.group(3)]
         return f"{m.group(1)}<{m.group(2)},{m.group(3)}> ({kind})"
     m = re.search(r"gemm_bwd_pair_kernelILi(\d)E", name) or re.search(r"gemm_bwd_pair_kernel<(?:\(int\))?(\d)[,>]", name)
     if m:

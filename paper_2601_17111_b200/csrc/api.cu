@@ -211,6 +211,8 @@ struct llep_context {
   size_t off_o = 0, off_grad = 0;
   uint16_t *gu = nullptr, *da0 = nullptr, *aw = nullptr, *dgu = nullptr;
   float *stage13 = nullptr, *stage2 = nullptr;
+  float *dotp = nullptr;    // fused dA0 + SwiGLU backward: partial <a, dA0> per (row, half tile)
+  int64_t dotp_cap = 0;     // floats
   float *wsbuf = nullptr;   // split-K partials of the weight-gradient GEMMs
   int64_t ws_cap = 0;       // floats
   uint8_t *peer_base[kMaxWorld] = {};
@@ -496,7 +498,7 @@ void llep_context_destroy(llep_context *c) {
   void *ptrs[] = {c->tile_cnt, c->tile_off, c->cnt, c->local_rank, c->slot_dst, c->err,
                   c->lm_local, c->rows_on, c->chunk_row, c->foreign_slot, c->dev_padded,
                   c->dev_foreign, c->groups, c->sched, c->summary, c->d_ptrs, c->act, c->arena,
-                  c->gu, c->da0, c->aw, c->dgu, c->stage13, c->stage2, c->wsbuf};
+                  c->gu, c->da0, c->aw, c->dgu, c->stage13, c->stage2, c->wsbuf, c->dotp};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->summary_host) cudaFreeHost(c->summary_host);
@@ -1069,11 +1071,43 @@ static llep_status moe_backward(llep_context *c, const uint16_t *x, const int32_
     b.out = c->da0;
     b.num_sms = c->num_sms;
     b.pair = getenv("LLEP_BWD_1CTA") ? 0 : 1;
-    if ((st = run_gemm_bwd(b, s)) != LLEP_OK) return st;
-    ++c->launches;
-    // SwiGLU backward per row; dL/dw replaces the gate in G
-    LLEP_CUDA(launch_bwd_swiglu(c->groups, G_, (int)sum.my_padded, H, GU, c->da0, G, c->aw, c->dgu, s));
-    ++c->launches;
+    // opt-in: dA0 GEMM with the SwiGLU backward fused into its epilogue.  Measured 11-15 % SLOWER per
+    // training step than dA0 + bwd_swiglu (its epilogue's per-row GU loads are latency-bound and
+    // outlast the tile's MMAs), so the separate kernel is the default
+    const char *fz = getenv("LLEP_BWD_FUSED");
+    const bool fuse = b.pair && fz && atoi(fz);
+    if (fuse) {
+      // dA0 GEMM with the SwiGLU backward in its epilogue (dA0 never reaches HBM): w·a, [dg | du] and
+      // per-tile partial dots; padding rows zeroed separately; dL/dw = fixed-order sum of the partials
+      const int nparts = 2 * ((H + 255) / 256);
+      const int64_t need = c->arena_rows * nparts;
+      if (need > c->dotp_cap) {
+        LLEP_CUDA(cudaStreamSynchronize(s));
+        if (c->dotp) cudaFree(c->dotp);
+        c->dotp = nullptr;
+        c->dotp_cap = 0;
+        LLEP_CUDA(cudaMalloc(&c->dotp, (size_t)need * 4));
+        c->dotp_cap = need;
+      }
+      b.kind = 2;
+      b.gu = GU;
+      b.gate = G;
+      b.aw = c->aw;
+      b.dgu = c->dgu;
+      b.dotp = c->dotp;
+      if ((st = run_gemm_bwd(b, s)) != LLEP_OK) return st;
+      LLEP_CUDA(launch_zero_pad(c->groups, G_, H, c->aw, nullptr, s));
+      LLEP_CUDA(launch_zero_pad(c->groups, G_, 2 * H, c->dgu, nullptr, s));
+      LLEP_CUDA(launch_dot_reduce(c->groups, G_, (int)sum.my_padded, nparts, c->dotp, G, s));
+      c->launches += 4;
+      b.kind = 0;
+    } else {
+      if ((st = run_gemm_bwd(b, s)) != LLEP_OK) return st;
+      ++c->launches;
+      // SwiGLU backward per row; dL/dw replaces the gate in G
+      LLEP_CUDA(launch_bwd_swiglu(c->groups, G_, (int)sum.my_padded, H, GU, c->da0, G, c->aw, c->dgu, s));
+      ++c->launches;
+    }
     // dW_down = dOᵀ · (w a)   and   dW13 = [dg|du]ᵀ · X   (native -> dw2/dw13, foreign -> staging);
     // large groups are split along their rows, partials summed in fixed order (deterministic)
     std::vector<int32_t> grows, gslot, gexp;

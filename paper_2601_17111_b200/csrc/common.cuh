@@ -140,6 +140,8 @@ cudaError_t launch_planner(const int32_t *load_matrix, int32_t N, int32_t P, dou
 cudaError_t launch_layout(const LayoutArgs &a, cudaStream_t s);
 cudaError_t launch_zero_pad(const Group *groups, int n_groups, int D, uint16_t *buf0, uint16_t *buf1,
                             cudaStream_t s);
+cudaError_t launch_dot_reduce(const Group *groups, int n_groups, int n_rows_total, int nparts, const float *dotp,
+                              float *gate_io, cudaStream_t s);
 cudaError_t launch_bwd_swiglu(const Group *groups, int n_groups, int n_rows_total, int H, const uint16_t *GU,
                               const uint16_t *dA0, float *gate_io, uint16_t *Aw, uint16_t *dGU, cudaStream_t s);
 cudaError_t launch_grad_reduce(float *dst, const float *base, int n_src, int64_t stride_floats, int64_t n_floats,
@@ -232,6 +234,11 @@ struct BwdArgs {
   void *out;
   int32_t num_sms;
   int32_t pair;               // 1: 2-CTA (cta_group::2) variant, 256-row / 256-output-row pair tiles
+  // kind 2 (= kind 0 for dA0 = dY·W_down, with the SwiGLU backward fused into the epilogue; pair only):
+  const uint16_t *gu;         //   [rows, 2*nout] saved / recomputed pre-activations [g | u]
+  const float *gate;          //   [rows] the row's gate w
+  uint16_t *aw, *dgu;         //   out: w·a [rows, nout], [dg | du] [rows, 2*nout]
+  float *dotp;                //   out: partial <a, dA0> per (row, 128-column half tile) [rows, 2*ceil(nout/256)]
 };
 llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s);
 

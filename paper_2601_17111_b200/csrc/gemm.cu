@@ -854,7 +854,7 @@ template <int KIND> struct BwdCfg {
 };
 
 struct BwdParams {
-  CUtensorMap tmA, tmB, tmB1;   // tmB1: foreign-expert weights (KIND 0, groups with wslot < 0)
+  CUtensorMap tmA, tmB, tmB1;   // tmB1: foreign-expert weights (KIND 0/2, groups with wslot < 0)
   CUtensorMap tmO, tmOF, tmWS;  // KIND 1 fp32 outputs, 3D {nout, mdim, slot}: out, out_foreign, ws
   const Group *groups;
   int32_t n_groups;
@@ -867,6 +867,10 @@ struct BwdParams {
   void *out_foreign;     // KIND 1: output of foreign groups (wslot < 0), nullptr -> out[expert]
   float *ws;             // KIND 1: split-K partials
   int32_t num_sms;       // scheduling units for the split heuristic (SMs, or CTA pairs)
+  const __nv_bfloat16 *gu;   // KIND 2: [g | u] rows, gates, outputs w·a, [dg | du], partial dots
+  const float *gate;
+  __nv_bfloat16 *aw, *dgu;
+  float *dotp;
 };
 
 __device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr) {
@@ -1162,7 +1166,7 @@ constexpr int kPairA = BM * BK * 2;        // 16 KB per CTA
 constexpr int kPairB = 128 * BK * 2;       // 16 KB per CTA (half of N)
 constexpr int kPairStage = kPairA + kPairB;
 template <int KIND> struct BwdPairCfg {
-  static constexpr int STAGES = KIND == 0 ? 6 : 4;
+  static constexpr int STAGES = KIND == 1 ? 4 : 6;
   static constexpr int SMEM = STAGES * kPairStage + 1024 + (KIND == 1 ? kBwdNStg * kBwdStg : kStoreStageBytes) + 1024;
 };
 
@@ -1170,7 +1174,7 @@ template <int KIND>
 __device__ __forceinline__ BwdTile decode_bwd_pair(int t, const BwdParams &p, const int *s_mblk) {
   BwdTile ti;
   ti.half = 0;
-  if (KIND == 0) {
+  if (KIND != 1) {
     const int mb = t / p.n_nt;
     ti.n0 = (t - mb * p.n_nt) * kBwdBN;
     int lo = 0, hi = p.n_groups - 1;
@@ -1233,7 +1237,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
-  if (KIND == 0) {
+  if (KIND != 1) {
     for (int g = threadIdx.x; g < p.n_groups; g += kGemmThreads) s_mblk[g] = p.groups[g].mblk_start;
   } else if (threadIdx.x == 0) {
     const int per = p.n_mt * p.n_nt;
@@ -1274,7 +1278,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
   const uint32_t tmem_base = *tmem_slot;
   int total_tiles = 0;
   if (p.n_groups > 0) {
-    if (KIND == 0) {
+    if (KIND != 1) {
       const Group last = p.groups[p.n_groups - 1];
       total_tiles = (last.mblk_start + (last.n_rows + 2 * BM - 1) / (2 * BM)) * p.n_nt;
     } else {
@@ -1289,9 +1293,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
       uint32_t phase = 0;
       for (int t = pair; t < total_tiles; t += n_pairs) {
         const BwdTile ti = decode_bwd_pair<KIND>(t, p, s_mblk);
-        const int ws = KIND == 0 ? p.groups[ti.g].wslot : 0;
+        const int ws = KIND != 1 ? p.groups[ti.g].wslot : 0;
         const int wrow = (ws >= 0 ? ws : -1 - ws) * p.kdim;
-        const CUtensorMap *bm = (KIND == 0 && ws < 0) ? &p.tmB1 : &p.tmB;
+        const CUtensorMap *bm = (KIND != 1 && ws < 0) ? &p.tmB1 : &p.tmB;
         for (int kb = 0; kb < ti.nk; ++kb) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const uint32_t fl = smem_u32(full + stage);
@@ -1299,7 +1303,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
           const uint32_t fb = mapa_shared(fl, 0);
           const uint32_t a_dst = smem_u32(sA + stage * kPairA);
           const uint32_t b_dst = smem_u32(sB + stage * kPairB);
-          if (KIND == 0) {
+          if (KIND != 1) {
             tma_load_2d_pair(a_dst, &p.tmA, fb, kb * BK, ti.row0 + (int)crank * (ti.half ? BM / 2 : BM), pol);
 #pragma unroll
             for (int c = 0; c < 2; ++c)
@@ -1329,7 +1333,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
       int it = 0;
       for (int t = pair; t < total_tiles; t += n_pairs, ++it) {
         const BwdTile ti = decode_bwd_pair<KIND>(t, p, s_mblk);
-        const uint32_t idesc = (KIND == 0 && ti.half) ? idesc_half : idesc_full;
+        const uint32_t idesc = (KIND != 1 && ti.half) ? idesc_half : idesc_full;
         const int acc = it & 1;
         mbar_wait(smem_u32(tempty + acc), ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -1341,7 +1345,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
           const uint32_t b0 = smem_u32(sB + stage * kPairB);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = KIND == 0 ? smem_desc(a0 + kk * 32) : smem_desc_mn(a0 + kk * 2048);
+            const uint64_t ad = KIND != 1 ? smem_desc(a0 + kk * 32) : smem_desc_mn(a0 + kk * 2048);
             tc_mma_pair(d_tmem, ad, smem_desc_mn(b0 + kk * 2048), idesc, (kb | kk) != 0);
           }
           tc_commit_pair(smem_u32(empty + stage));
@@ -1362,7 +1366,94 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
       mbar_wait(smem_u32(tfull + acc), (it >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
-      if (KIND == 0) {
+      if (KIND == 2) {
+        // dA0 tile + SwiGLU backward (row f1): per element with g, u from GU and d = dA0 (fp32, TMEM)
+        //   a = silu(g) u, da = w d, dg = da u sg (1 + g (1 - sg)), du = da silu(g), dot += a d
+        // writes w·a, dg, du (bf16) and this thread's partial <a, dA0> over its columns
+        const int L = q * 32 + lane;
+        const int row = ti.half ? ti.row0 + (int)crank * (BM / 2) + (L & 63) : ti.row0 + (int)crank * BM + L;
+        const int c0 = ti.half ? (L >> 6) * (kBwdBN / 2) : 0, cw = ti.half ? kBwdBN / 2 : kBwdBN;
+        const bool ok = row < ti.row_end;
+        const int H = p.nout;
+        const float w = ok ? p.gate[row] : 0.f;
+        const __nv_bfloat16 *gurow = p.gu + (size_t)row * 2 * H + ti.n0 + c0;
+        __nv_bfloat16 *awrow = p.aw + (size_t)row * H + ti.n0 + c0;
+        __nv_bfloat16 *dgrow = p.dgu + (size_t)row * 2 * H + ti.n0 + c0;
+        uint8_t *wst = reinterpret_cast<uint8_t *>(stg) + q * (32 * 128);
+        float dot = 0.f;
+#pragma unroll 1
+        for (int j = 0; j < cw; j += 32) {
+          const int left = (H - ti.n0 - c0 - j) / 8;
+          const int nv = left < 4 ? (left > 0 ? left : 0) : 4;
+          float v[32];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tmem_ld8(taddr + j + 8 * c, v + 8 * c);
+          uint4 gv[4], uv[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            gv[c] = make_uint4(0, 0, 0, 0);
+            uv[c] = make_uint4(0, 0, 0, 0);
+            if (ok && c < nv) {
+              gv[c] = __ldg(reinterpret_cast<const uint4 *>(gurow + j + 8 * c));
+              uv[c] = __ldg(reinterpret_cast<const uint4 *>(gurow + H + j + 8 * c));
+            }
+          }
+          tmem_ld_wait();
+          uint4 oa[8], og[8], ou[8];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const __nv_bfloat162 *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gv[c]);
+            const __nv_bfloat162 *u2 = reinterpret_cast<const __nv_bfloat162 *>(&uv[c]);
+            __nv_bfloat162 *a2 = reinterpret_cast<__nv_bfloat162 *>(&oa[c]);
+            __nv_bfloat162 *gg = reinterpret_cast<__nv_bfloat162 *>(&og[c]);
+            __nv_bfloat162 *uu = reinterpret_cast<__nv_bfloat162 *>(&ou[c]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 gf = __bfloat1622float2(g2[i]), uf = __bfloat1622float2(u2[i]);
+              const float gz[2] = {gf.x, gf.y}, uz[2] = {uf.x, uf.y};
+              float ar[2], dgr[2], dur[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const float d = v[8 * c + 2 * i + e];
+                const float sg = 1.f / (1.f + __expf(-gz[e]));
+                const float si = gz[e] * sg;
+                const float a = si * uz[e];
+                const float da = w * d;
+                ar[e] = w * a;
+                dot += a * d;
+                dgr[e] = da * uz[e] * sg * (1.f + gz[e] * (1.f - sg));
+                dur[e] = da * si;
+              }
+              a2[i] = __floats2bfloat162_rn(ar[0], ar[1]);
+              gg[i] = __floats2bfloat162_rn(dgr[0], dgr[1]);
+              uu[i] = __floats2bfloat162_rn(dur[0], dur[1]);
+            }
+          }
+          if (!ti.half) {
+            const int k = ok ? 1 : 0;
+            warp_store_rows(wst, lane, oa, nv, reinterpret_cast<unsigned long long>(awrow + j), k);
+            warp_store_rows(wst, lane, og, nv, reinterpret_cast<unsigned long long>(dgrow + j), k);
+            warp_store_rows(wst, lane, ou, nv, reinterpret_cast<unsigned long long>(dgrow + H + j), k);
+          } else if (ok) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (c < nv) {
+                *reinterpret_cast<uint4 *>(awrow + j + 8 * c) = oa[c];
+                *reinterpret_cast<uint4 *>(dgrow + j + 8 * c) = og[c];
+                *reinterpret_cast<uint4 *>(dgrow + H + j + 8 * c) = ou[c];
+              }
+          }
+        }
+        if (ok) {   // partial dots: slot 2·nb + (128-column half); a full tile leaves its second slot 0
+          float *dp = p.dotp + (size_t)row * (2 * p.n_nt) + 2 * (ti.n0 / kBwdBN);
+          if (ti.half) {
+            dp[L >> 6] = dot;
+          } else {
+            dp[0] = dot;
+            dp[1] = 0.f;
+          }
+        }
+      } else if (KIND == 0) {
         // full tile: lane = row of this CTA's 128; half tile (M=128 pair MMA): lanes 0-63 hold
         // columns [0, 128) and lanes 64-127 columns [128, 256) of the CTA's 64 rows
         const int L = q * 32 + lane;
@@ -1565,8 +1656,19 @@ llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s) {
   p.out_foreign = a.out_foreign;
   p.ws = a.ws;
   p.num_sms = a.pair ? a.num_sms / 2 : a.num_sms;
+  if (a.kind == 2) {
+    if (!a.pair || !a.gu || !a.gate || !a.aw || !a.dgu || !a.dotp) {
+      set_error("fused dA0 + SwiGLU-backward GEMM needs the pair kernel and all of gu, gate, aw, dgu, dotp");
+      return LLEP_ERR_INVALID;
+    }
+    p.gu = reinterpret_cast<const __nv_bfloat16 *>(a.gu);
+    p.gate = a.gate;
+    p.aw = reinterpret_cast<__nv_bfloat16 *>(a.aw);
+    p.dgu = reinterpret_cast<__nv_bfloat16 *>(a.dgu);
+    p.dotp = a.dotp;
+  }
   bool ok;
-  if (a.kind == 0) {
+  if (a.kind != 1) {
     ok = make_map_box(&p.tmA, a.a, a.rows, a.kdim, BK, BM) &&
          make_map_box(&p.tmB, a.b, (int64_t)a.n_weights * a.kdim, a.nout, 64, BK) &&
          make_map_box(&p.tmB1, a.b_foreign ? a.b_foreign : a.b,
@@ -1586,9 +1688,9 @@ llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s) {
     return LLEP_ERR_CUDA;
   }
   if (a.pair) {
-    static bool pattr[2] = {false, false};
-    auto kern = a.kind == 0 ? gemm_bwd_pair_kernel<0> : gemm_bwd_pair_kernel<1>;
-    const int smem = a.kind == 0 ? BwdPairCfg<0>::SMEM : BwdPairCfg<1>::SMEM;
+    static bool pattr[3] = {false, false, false};
+    auto kern = a.kind == 0 ? gemm_bwd_pair_kernel<0> : a.kind == 1 ? gemm_bwd_pair_kernel<1> : gemm_bwd_pair_kernel<2>;
+    const int smem = a.kind == 0 ? BwdPairCfg<0>::SMEM : a.kind == 1 ? BwdPairCfg<1>::SMEM : BwdPairCfg<2>::SMEM;
     if (!pattr[a.kind]) {
       LLEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       pattr[a.kind] = true;

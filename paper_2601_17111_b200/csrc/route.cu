@@ -486,6 +486,34 @@ cudaError_t launch_zero_pad(const Group *groups, int n_groups, int D, uint16_t *
   return cudaGetLastError();
 }
 
+// dL/dw of each real received row from the fused dA0 + SwiGLU-backward epilogue's per-tile partial
+// dot products <a, dA0> (nparts per row, summed in fixed order: deterministic); replaces the gate.
+__global__ void dot_reduce_kernel(const Group *__restrict__ groups, int n_groups, int n_rows_total, int nparts,
+                                  const float *__restrict__ dotp, float *__restrict__ gate_io) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rows_total) return;
+  int lo = 0, hi = n_groups - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (groups[mid].row_base <= r) lo = mid;
+    else hi = mid - 1;
+  }
+  const Group g = groups[lo];
+  if (r < g.row_base || r >= g.row_base + g.n_rows) return;
+  const float *q = dotp + (int64_t)r * nparts;
+  float acc = 0.f;
+  for (int j = 0; j < nparts; ++j) acc += q[j];
+  gate_io[r] = acc;
+}
+
+cudaError_t launch_dot_reduce(const Group *groups, int n_groups, int n_rows_total, int nparts, const float *dotp,
+                              float *gate_io, cudaStream_t s) {
+  if (n_rows_total <= 0 || n_groups <= 0) return cudaSuccess;
+  dot_reduce_kernel<<<(n_rows_total + 255) / 256, 256, 0, s>>>(groups, n_groups, n_rows_total, nparts, dotp,
+                                                               gate_io);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bwd_swiglu(const Group *groups, int n_groups, int n_rows_total, int H, const uint16_t *GU,
                               const uint16_t *dA0, float *gate_io, uint16_t *Aw, uint16_t *dGU, cudaStream_t s) {
   if (n_rows_total <= 0 || n_groups <= 0) return cudaSuccess;

@@ -194,3 +194,36 @@ def test_training_forward_saved_preactivations(L, cfg):
         ctx.forward_train(x, ids, gates, w13, w2, plan, gu=gu[:1])
     assert ei.value.code == 1
     ctx.close()
+
+
+@pytest.mark.parametrize("cfg", [("tiny", 95, 1), ((16, 4, 512, 360, 6000), 95, 1)])
+def test_backward_fused_swiglu_epilogue(L, cfg, monkeypatch):
+    """The opt-in dA0 GEMM with the SwiGLU backward fused into its epilogue (LLEP_BWD_FUSED=1) against
+    the default dA0 + bwd_swiglu path: same gradients up to the bf16 rounding of dA0 that the fused
+    path skips (dgates: fixed-order sum of per-tile partial dots)."""
+    name, pct, nhot = cfg
+    if isinstance(name, str):
+        base = W.CONFIGS[name]
+        sh = W.LayerShape(base.n_experts, base.top_k, base.d_model, base.d_ff, base.tokens_per_rank, 1)
+    else:
+        sh = W.LayerShape(*name, 1)
+    seed = 31
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, pct, nhot, seed, "cuda")
+    dout = torch.from_numpy(_dout(sh, 0, seed).view(np.int16)).cuda().view(torch.bfloat16)
+    ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, 1, 0, 0, sh.tokens_per_rank)
+    ctx.enable_backward()
+    plan, _ = ctx.prepare(ids)
+    ref = [t.float().cpu().numpy() for t in ctx.backward(x, ids, gates, dout, w13, w2, plan)]
+    monkeypatch.setenv("LLEP_BWD_FUSED", "1")
+    got = [t.float().cpu().numpy() for t in ctx.backward(x, ids, gates, dout, w13, w2, plan)]
+    torch.cuda.synchronize()
+    for a, b, n in zip(got, ref, ("dx", "dgates", "dw13", "dw2")):
+        mr, l2 = _rel(a, b)
+        assert mr <= 2e-2 and l2 <= 5e-3, (n, mr, l2)
+    if name == "tiny":
+        from oracle import backward as O5
+        ws = LC.OracleWeights(sh.d_model, sh.d_ff, seed)
+        xr = W.bf16_bits_to_f64(W.tokens_bits(sh.tokens_per_rank, sh.d_model, 0, seed))
+        dx, dg, dW = O5.moe_backward(xr, ids_np, g_np.astype(np.float64), W.bf16_bits_to_f64(_dout(sh, 0, seed)), ws)
+        _check_grads(sh, got, dx, dg, dW, range(sh.n_experts), 0)
+    ctx.close()

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--hot", type=int, default=95)
     ap.add_argument("--secs", type=float, default=3.0)
     ap.add_argument("--reps", type=int, default=4)
+    ap.add_argument("--train", action="store_true",
+                    help="time a training step: prepare + forward_train + backward from the saved [g|u]")
     args = ap.parse_args()
     base = W.CONFIGS[args.config]
     sh = W.LayerShape(base.n_experts, base.top_k, base.d_model, base.d_ff, base.tokens_per_rank, 1)
@@ -41,17 +43,31 @@ def main():
     out = torch.empty_like(x)
     plan_buf = torch.empty(L.plan_bytes(sh.n_experts, 1), dtype=torch.uint8, device=dev)
     outs = {}
+    if args.train:
+        ctx.enable_backward()
+        dout = W.tokens_torch(sh.tokens_per_rank, sh.d_model, 1000, dev, seed)
+        M, D, H = sh.experts_per_rank, sh.d_model, sh.d_ff
+        dx, dg = torch.empty_like(x), torch.empty(ids.shape, dtype=torch.float32, device=dev)
+        dw13 = torch.empty((M, 2 * H, D), dtype=torch.float32, device=dev)
+        dw2 = torch.empty((M, D, H), dtype=torch.float32, device=dev)
+        gu = [None]
 
     def batch(val):
         os.environ[args.var] = val
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.reps):
-            plan, _ = ctx.prepare(ids, plan_out=plan_buf)
-            ctx.forward(x, ids, gates, w13, w2, plan, out)
+            plan, req = ctx.prepare(ids, plan_out=plan_buf)
+            if args.train:
+                if gu[0] is None:
+                    gu[0] = torch.empty((int(req.rows_needed), 2 * sh.d_ff), dtype=torch.bfloat16, device=dev)
+                ctx.forward_train(x, ids, gates, w13, w2, plan, out, gu[0])
+                ctx.backward(x, ids, gates, dout, w13, w2, plan, dx, dg, dw13, dw2, gu=gu[0])
+            else:
+                ctx.forward(x, ids, gates, w13, w2, plan, out)
         e1.record()
         torch.cuda.synchronize()
-        outs[val] = out.clone()
+        outs[val] = (dx if args.train else out).clone()
         return e0.elapsed_time(e1) / args.reps
 
     for v in (args.a, args.b):

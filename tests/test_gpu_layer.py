@@ -182,21 +182,25 @@ def test_g120_p1_sampled_parity(L):
     ctx.close()
 
 
-@pytest.mark.parametrize("pct,nhot", [(95, 1), (0, 0)])
-def test_g120_p8_processes_one_gpu(L, tmp_path, pct, nhot):
-    """G120 at its N=8 launch configuration: 8 ranks (processes sharing cuda:0, CUDA-IPC arenas),
-    32K tokens/rank, λ=1.3 α=1 m=1024.  Plan == oracle on every rank, 7 weight transfers at 95 %/1
-    (EP fallback when balanced), sampled outputs vs O3, LLEP == EP bitwise on every full output."""
+@pytest.mark.parametrize("cfg,P,pct,nhot,n_tr", [
+    ("g120", 8, 95, 1, 7), ("g120", 8, 0, 0, 0),       # the north-star layer at its N=8 configuration
+    ("g20", 8, 95, 1, 7),                              # BASELINE configs[1]
+    ("g120", 4, 95, 4, 5), ("g120", 2, 95, 16, 8),     # SWEEP rows at EP 4 / EP 2
+])
+def test_large_layer_processes_one_gpu(L, tmp_path, cfg, P, pct, nhot, n_tr):
+    """BASELINE shapes at full size with P ranks (processes sharing cuda:0, CUDA-IPC arenas),
+    λ=1.3 α=1 m=1024.  Plan == oracle on every rank (expected weight-transfer count; EP fallback when
+    balanced), sampled outputs vs O3, LLEP == EP bitwise on every full output."""
     from oracle import planner as O1
     from oracle import schedule as O2
-    P, S = 8, 48
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29600 + pct))
-    cmd = [sys.executable, os.path.join(HERE, "mp_layer_worker.py"), str(P), "g120", str(pct), str(nhot),
+    S = 48
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29600 + pct + 7 * P + len(cfg)))
+    cmd = [sys.executable, os.path.join(HERE, "mp_layer_worker.py"), str(P), cfg, str(pct), str(nhot),
            str(tmp_path), str(S)]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1500)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = [np.load(os.path.join(tmp_path, f"rank{p}.npz")) for p in range(P)]
-    sh0 = W.CONFIGS["g120"]
+    sh0 = W.CONFIGS[cfg]
     sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, P)
     hot = None if pct == 0 else pct
     ids_all = [W.routing_ids(sh, p, hot, nhot, 21) for p in range(P)]
@@ -206,7 +210,7 @@ def test_g120_p8_processes_one_gpu(L, tmp_path, pct, nhot):
     assert all(p == plans[0] for p in plans)
     dp = L.parse_plan(plans[0])
     assert [list(A) for A in dp.chunks] == [list(A) for A in ref_plan.chunks]
-    assert len(ref_plan.transfers) == (7 if pct else 0) and dp.fallback == (pct == 0)
+    assert len(ref_plan.transfers) == n_tr and dp.fallback == (pct == 0)
     w = LC.OracleWeights(sh.d_model, sh.d_ff, 21)
     rows = np.arange(S)
     for p in range(P):

@@ -1419,6 +1419,7 @@ llep_status llep_gemm_bwd(int32_t kind, const uint16_t *a, const uint16_t *w_or_
   ba.mblk_scale = 2;   // Group.mblk_start counts 256-row blocks
   ba.out = out;
   ba.num_sms = sms;
+  if (const char *o = getenv("LLEP_GEMM_SMS")) ba.num_sms = std::max(2, std::min(sms, atoi(o)));   // experiments
   ba.pair = pair;
   std::vector<int32_t> nr(n_groups), ex(n_groups);
   for (int i = 0; i < n_groups; ++i) {

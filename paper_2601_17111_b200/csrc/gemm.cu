@@ -1165,9 +1165,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_kernel(const __grid_
 constexpr int kPairA = BM * BK * 2;        // 16 KB per CTA
 constexpr int kPairB = 128 * BK * 2;       // 16 KB per CTA (half of N)
 constexpr int kPairStage = kPairA + kPairB;
+#ifndef LLEP_BWD_KSUB
+#define LLEP_BWD_KSUB 2   // A/B: build with -DLLEP_BWD_KSUB=1 for 64-deep stages in the row kinds
+#endif
 template <int KIND> struct BwdPairCfg {
-  static constexpr int STAGES = KIND == 1 ? 4 : 6;
-  static constexpr int SMEM = STAGES * kPairStage + 1024 + (KIND == 1 ? kBwdNStg * kBwdStg : kStoreStageBytes) + 1024;
+  // row kinds: two 64-deep K sub-tiles per pipeline stage (8 MMAs per barrier round trip, as in the
+  // forward); the weight-gradient kind keeps 64-deep stages (a small group is one K step)
+  static constexpr int KSUB = KIND == 1 ? 1 : (LLEP_BWD_KSUB);
+  static constexpr int STAGES = KIND == 1 ? 4 : 6 / KSUB;
+  static constexpr int SMEM = STAGES * KSUB * kPairStage + 1024 + (KIND == 1 ? kBwdNStg * kBwdStg : kStoreStageBytes) + 1024;
 };
 
 template <int KIND>
@@ -1223,15 +1229,16 @@ __device__ __forceinline__ BwdTile decode_bwd_pair(int t, const BwdParams &p, co
 template <int KIND>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __grid_constant__ BwdParams p) {
   constexpr int S = BwdPairCfg<KIND>::STAGES;
+  constexpr int KS = BwdPairCfg<KIND>::KSUB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
   uint8_t *sA = smem;
-  uint8_t *sB = smem + S * kPairA;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S * kPairStage);
+  uint8_t *sB = smem + S * KS * kPairA;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S * KS * kPairStage);
   uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tempty = bars + 2 * S + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
-  float *stg = reinterpret_cast<float *>(smem + S * kPairStage + 1024);
+  float *stg = reinterpret_cast<float *>(smem + S * KS * kPairStage + 1024);
   int ep_chunk = 0;
   __shared__ int s_mblk[kMaxGroups + 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1296,13 +1303,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
         const int ws = KIND != 1 ? p.groups[ti.g].wslot : 0;
         const int wrow = (ws >= 0 ? ws : -1 - ws) * p.kdim;
         const CUtensorMap *bm = (KIND != 1 && ws < 0) ? &p.tmB1 : &p.tmB;
-        for (int kb = 0; kb < ti.nk; ++kb) {
+        for (int kq = 0; kq * KS < ti.nk; ++kq) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
+          const int nsub = min(KS, ti.nk - kq * KS);
           const uint32_t fl = smem_u32(full + stage);
-          if (leader) mbar_expect_tx(fl, 2 * kPairStage);
+          if (leader) mbar_expect_tx(fl, 2 * nsub * kPairStage);
           const uint32_t fb = mapa_shared(fl, 0);
-          const uint32_t a_dst = smem_u32(sA + stage * kPairA);
-          const uint32_t b_dst = smem_u32(sB + stage * kPairB);
+          for (int s2 = 0; s2 < nsub; ++s2) {
+          const int kb = kq * KS + s2;
+          const uint32_t a_dst = smem_u32(sA + (stage * KS + s2) * kPairA);
+          const uint32_t b_dst = smem_u32(sB + (stage * KS + s2) * kPairB);
           if (KIND != 1) {
             tma_load_2d_pair(a_dst, &p.tmA, fb, kb * BK, ti.row0 + (int)crank * (ti.half ? BM / 2 : BM), pol);
 #pragma unroll
@@ -1315,6 +1325,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
 #pragma unroll
             for (int c = 0; c < 2; ++c)
               tma_load_2d_pair(b_dst + c * 8192, &p.tmB, fb, ti.n0 + (int)crank * 128 + c * 64, ti.row0 + kb * BK, pol);
+          }
           }
           if (++stage == S) {
             stage = 0;
@@ -1338,15 +1349,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
         mbar_wait(smem_u32(tempty + acc), ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
-        for (int kb = 0; kb < ti.nk; ++kb) {
+        for (int kq = 0; kq * KS < ti.nk; ++kq) {
           mbar_wait(smem_u32(full + stage), phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * kPairA);
-          const uint32_t b0 = smem_u32(sB + stage * kPairB);
+          const int nsub = min(KS, ti.nk - kq * KS);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = KIND != 1 ? smem_desc(a0 + kk * 32) : smem_desc_mn(a0 + kk * 2048);
-            tc_mma_pair(d_tmem, ad, smem_desc_mn(b0 + kk * 2048), idesc, (kb | kk) != 0);
+          for (int s2 = 0; s2 < KS; ++s2) {
+            if (s2 < nsub) {
+              const int kb = kq * KS + s2;
+              const uint32_t a0 = smem_u32(sA + (stage * KS + s2) * kPairA);
+              const uint32_t b0 = smem_u32(sB + (stage * KS + s2) * kPairB);
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk) {
+                const uint64_t ad = KIND != 1 ? smem_desc(a0 + kk * 32) : smem_desc_mn(a0 + kk * 2048);
+                tc_mma_pair(d_tmem, ad, smem_desc_mn(b0 + kk * 2048), idesc, (kb | kk) != 0);
+              }
+            }
           }
           tc_commit_pair(smem_u32(empty + stage));
           if (++stage == S) {

@@ -37,6 +37,10 @@ struct GemmParams {
   CUtensorMap tmA;     // activations [rows, kdim]
   CUtensorMap tmW0;    // native weights [n_native * wrows, kdim]
   CUtensorMap tmW1;    // foreign weights [n_foreign * wrows, kdim]
+  CUtensorMap tmAs;    // pair kernel, swapped tiles: activations, 32-row boxes (the N operand)
+  CUtensorMap tmW0s;   //   native weights, 64-row boxes (the M operand)
+  CUtensorMap tmW1s;   //   foreign weights, 64-row boxes
+  int32_t swap;        // pair kernel: groups of <= 64 rows run as swapped tiles (weights x tokens)
   const Group *groups;
   const int32_t *sched;
   const int32_t *n_groups_dev;
@@ -87,6 +91,7 @@ __device__ __forceinline__ uint32_t instr_desc() {
 struct TileInfo {
   int row0, row_end, nb, wslot, small;
   int half;   // pair kernel: <= 128 rows left in this block -> M=128 pair MMA (64 rows per CTA)
+  int swap;   // pair kernel: <= 64 rows -> swapped tile, D[weight rows x tokens] (M=256, N=64)
 };
 
 template <int TM = BM>
@@ -117,6 +122,7 @@ __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int *
   ti.wslot = g.wslot;
   ti.small = g.n_rows <= kSmallGroupRows;  // its weights are streamed once: evict first from L2
   ti.half = ti.row_end - ti.row0 <= TM / 2;
+  ti.swap = 0;
   return ti;
 }
 
@@ -435,15 +441,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < total_tiles; t += n_pairs) {
-        const TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
+        TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
+        ti.swap = p.swap && ti.row_end - ti.row0 <= 64;
         const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
         const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
         const int brow = MODE != 1 ? wbase + (int)crank * p.wup_off : wbase + (int)crank * (BN / 2);
         wait_weights(p, ti.wslot);
+        // swapped tile: this CTA's 128 weight rows as the A operand (mode 0/2/3: 64 gate + the
+        // matching 64 up rows of features nb*BNO + crank*64 ...; mode 1: rows nb*BN + crank*BN/2
+        // ...) and its 32 of the group's <= 64 token rows as the B operand
+        const CUtensorMap *wms = ti.wslot >= 0 ? &p.tmW0s : &p.tmW1s;
+        const int srow = MODE != 1 ? wbase + (int)crank * 64 : wbase + (int)crank * (BN / 2);
+        const int srow2 = MODE != 1 ? srow + p.wup_off : srow + 64;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const int nsub = min(KSUB, (p.kdim - kb * KST + BK - 1) / BK);   // skip all-OOB sub-tiles
           const uint32_t fl = smem_u32(full + stage);
+          if (ti.swap) {
+            if (leader) mbar_expect_tx(fl, 2 * nsub * (BM * 128 + 32 * 128));
+            const uint32_t fb = mapa_shared(fl, 0);
+            for (int s2 = 0; s2 < nsub; ++s2) {
+              const uint32_t ad = smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128));
+              tma_load_2d_pair(ad, wms, fb, (kb * KSUB + s2) * BK, srow, ti.small ? pol_first : pol_last);
+              tma_load_2d_pair(ad + 64 * 128, wms, fb, (kb * KSUB + s2) * BK, srow2, ti.small ? pol_first : pol_last);
+              tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES + s2 * ((BN / 2) * 128)), &p.tmAs, fb,
+                               (kb * KSUB + s2) * BK, ti.row0 + (int)crank * 32, pol_act);
+            }
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           if (leader) mbar_expect_tx(fl, 2 * nsub * (C::STAGE / KSUB));
           const uint32_t fb = mapa_shared(fl, 0);
           for (int s2 = 0; s2 < nsub; ++s2) {
@@ -467,6 +496,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
                                   ((uint32_t)(TM >> 4) << 24);
       const uint32_t idesc_half = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                   ((uint32_t)((TM / 2) >> 4) << 24);
+      const uint32_t idesc_swap = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) |
+                                  ((uint32_t)(TM >> 4) << 24);
       const uint64_t adesc0 = smem_desc(smem_u32(sA)), bdesc0 = smem_desc(smem_u32(sB));
       int stage = 0;
       uint32_t phase = 0;
@@ -474,8 +505,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       for (int t = pair; t < total_tiles; t += n_pairs, ++it) {
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
-        const TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
-        const uint32_t idesc = ti.half ? idesc_half : idesc_full;
+        TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
+        ti.swap = p.swap && ti.row_end - ti.row0 <= 64;
+        const uint32_t idesc = ti.swap ? idesc_swap : ti.half ? idesc_half : idesc_full;
         mbar_wait(smem_u32(tempty + acc), aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
@@ -513,7 +545,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
     for (int t = pair; t < total_tiles; t += n_pairs, ++it) {
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      const TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
+      TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
+        ti.swap = p.swap && ti.row_end - ti.row0 <= 64;
       mbar_wait(smem_u32(tfull + acc), aphase);
       tc_fence_after();
       const int row = ti.row0 + (int)crank * BM + q * 32 + lane;
@@ -521,7 +554,83 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
       const int col0 = ti.nb * BNO;
       constexpr int bno = BNO;
-      if (ti.half) {
+      if (ti.swap) {
+        // swapped tile: TMEM lane L = weight row (feature) of this CTA, column j = token row0 + j
+        const int L = q * 32 + lane;
+        if (MODE == 1) {
+          const int fl = L;                                   // this CTA's rows nb*BN + crank*BN/2 + L
+          const int d = ti.nb * BN + (int)crank * (BN / 2) + fl;
+          const bool fok = fl < BN / 2 && d < p.nout;
+#pragma unroll 1
+          for (int j = 0; j < 64; j += 8) {
+            float v[8];
+            tmem_ld8(taddr + j, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int row = ti.row0 + j + i;
+              if (fok && row < ti.row_end) {
+                __nv_bfloat16 *orow = p.out + (size_t)row * p.nout;
+                if (p.peer_slot) {
+                  const int32_t src = p.row_src[row];
+                  orow = reinterpret_cast<__nv_bfloat16 *>(p.peer_slot[src & 31]) + (size_t)(src >> 5) * p.nout;
+                }
+                orow[d] = __float2bfloat16_rn(p.gate[row] * v[i]);
+              }
+            }
+          }
+        } else {
+          // lanes 0-63: gate rows of features f0 + L, lanes 64-127: the matching up rows
+          const int hi = L >> 6, fl = L & 63;
+          const int fr = (int)crank * 64 + fl;               // feature within the tile's BNO
+          const int f = ti.nb * BNO + fr;
+          const bool fok = fr < BNO && f < p.nout;
+          if (MODE == 2 || MODE == 3) {   // raw [g | u] rows
+            __nv_bfloat16 *gdst = (MODE == 2 ? p.out : p.out2) + (size_t)hi * p.nout + f;
+#pragma unroll 1
+            for (int j = 0; j < 64; j += 8) {
+              float v[8];
+              tmem_ld8(taddr + j, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (fok && ti.row0 + j + i < ti.row_end)
+                  gdst[(size_t)(ti.row0 + j + i) * 2 * p.nout] = __float2bfloat16_rn(v[i]);
+            }
+          }
+          if (MODE == 0 || MODE == 3) {
+            // SwiGLU: gate lanes finish tokens [0, 32), up lanes tokens [32, 64); each sends the
+            // other half of its 64 columns through shared memory ([2][64 features][33])
+            float *xs = xchg;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll 1
+            for (int jj = 0; jj < 32; jj += 8) {
+              float v[8];
+              tmem_ld8(taddr + (hi == 0 ? 32 : 0) + jj, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 8; ++i) xs[(hi * 64 + fl) * 33 + jj + i] = v[i];
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int jb = hi == 0 ? 0 : 32;
+#pragma unroll 1
+            for (int jj = 0; jj < 32; jj += 8) {
+              float v[8];
+              tmem_ld8(taddr + jb + jj, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float o = xs[((1 - hi) * 64 + fl) * 33 + jj + i];
+                const float g = hi == 0 ? v[i] : o, u = hi == 0 ? o : v[i];
+                const int row = ti.row0 + jb + jj + i;
+                if (fok && row < ti.row_end)
+                  p.out[(size_t)row * p.nout + f] = __float2bfloat16_rn(__fdividef(g, 1.f + __expf(-g)) * u);
+              }
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+          }
+        }
+      } else if (ti.half) {
         // M=128 pair tile: this CTA's 64 rows.  TMEM lanes 0-63 hold accumulator columns [0, BN/2)
         // (the B rows staged by CTA 0) and lanes 64-127 columns [BN/2, BN) (CTA 1's) of the SAME
         // 64 rows, both at TMEM columns 0 .. BN/2-1.
@@ -810,6 +919,13 @@ llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
       !make_map(&prm.tmW1, g.w_foreign ? g.w_foreign : g.w_native,
                 (int64_t)(g.w_foreign ? g.n_foreign : g.n_native) * wrows, g.kdim, box_w)) {
     set_error("cuTensorMapEncodeTiled failed (alignment: kdim %% 8 == 0, 16-byte aligned bases)");
+    return LLEP_ERR_CUDA;
+  }
+  if (!make_map(&prm.tmAs, g.a, g.a_rows, g.kdim, 32) ||
+      !make_map(&prm.tmW0s, g.w_native, (int64_t)g.n_native * wrows, g.kdim, 64) ||
+      !make_map(&prm.tmW1s, g.w_foreign ? g.w_foreign : g.w_native,
+                (int64_t)(g.w_foreign ? g.n_foreign : g.n_native) * wrows, g.kdim, 64)) {
+    set_error("cuTensorMapEncodeTiled failed (swapped-tile maps)");
     return LLEP_ERR_CUDA;
   }
   prm.wrows = wrows;
@@ -1770,6 +1886,10 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   prm.gate = g.gate;
   prm.out = reinterpret_cast<__nv_bfloat16 *>(g.out);
   prm.out2 = reinterpret_cast<__nv_bfloat16 *>(g.out2);
+  {
+    const char *sw = getenv("LLEP_GEMM_SWAP");   // A/B switch: swapped tiles for groups of <= 64 rows
+    prm.swap = sw ? atoi(sw) : 1;
+  }
   if (g.mode == 3 && !g.out2) {
     set_error("grouped GEMM mode 3 needs the pre-activation output");
     return LLEP_ERR_INVALID;

@@ -1281,6 +1281,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_kernel(const __grid_
 constexpr int kPairA = BM * BK * 2;        // 16 KB per CTA
 constexpr int kPairB = 128 * BK * 2;       // 16 KB per CTA (half of N)
 constexpr int kPairStage = kPairA + kPairB;
+#ifndef LLEP_WG_NSTG
+#define LLEP_WG_NSTG 4    // pair weight-gradient epilogue: fp32 staging buffers (TMA stores in flight)
+#endif
+#ifndef LLEP_WG_STAGES
+#define LLEP_WG_STAGES 4  // pair weight-gradient kernel: operand pipeline stages
+#endif
+constexpr int kPairNStg = LLEP_WG_NSTG;
 #ifndef LLEP_BWD_KSUB
 #define LLEP_BWD_KSUB 2   // A/B: build with -DLLEP_BWD_KSUB=1 for 64-deep stages in the row kinds
 #endif
@@ -1288,8 +1295,8 @@ template <int KIND> struct BwdPairCfg {
   // row kinds: two 64-deep K sub-tiles per pipeline stage (8 MMAs per barrier round trip, as in the
   // forward); the weight-gradient kind keeps 64-deep stages (a small group is one K step)
   static constexpr int KSUB = KIND == 1 ? 1 : (LLEP_BWD_KSUB);
-  static constexpr int STAGES = KIND == 1 ? 4 : 6 / KSUB;
-  static constexpr int SMEM = STAGES * KSUB * kPairStage + 1024 + (KIND == 1 ? kBwdNStg * kBwdStg : kStoreStageBytes) + 1024;
+  static constexpr int STAGES = KIND == 1 ? LLEP_WG_STAGES : 6 / KSUB;
+  static constexpr int SMEM = STAGES * KSUB * kPairStage + 1024 + (KIND == 1 ? kPairNStg * kBwdStg : kStoreStageBytes) + 1024;
 };
 
 template <int KIND>
@@ -1651,8 +1658,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
         const int m0 = ti.m0 + (int)crank * BM;
 #pragma unroll 1
         for (int c = 0; c < kBwdBN / 32; ++c, ++ep_chunk) {
-          const int b = ep_chunk % kBwdNStg;
-          if (lead) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+          const int b = ep_chunk % kPairNStg;
+          if (lead) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kPairNStg - 1) : "memory");
           asm volatile("bar.sync 2, 128;" ::: "memory");
           float v[32];
 #pragma unroll

@@ -23,6 +23,10 @@
 #include "common.cuh"
 #include "tc.cuh"
 
+#ifndef LLEP_SWAP_K
+#define LLEP_SWAP_K 3   // K sub-tiles per stage of a swapped tile (A/B: -DLLEP_SWAP_K=2)
+#endif
+
 namespace llep {
 
 namespace {
@@ -383,6 +387,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
   constexpr int S = C::STAGES;
   constexpr int TM = 2 * BM;                     // rows per pair tile
   constexpr int BNO = MODE != 1 ? BN / 2 : BN;   // output columns per tile
+  // swapped tiles carry 3 K sub-tiles per stage when the stage has room (A 16 KB + B 4 KB each; the
+  // third A sub-tile goes into the B region): 50 % more weight bytes in flight for these HBM-fed tiles
+  constexpr int SWK = C::B_BYTES >= BM * 128 + 3 * 32 * 128 ? LLEP_SWAP_K : 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -453,26 +460,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
         const CUtensorMap *wms = ti.wslot >= 0 ? &p.tmW0s : &p.tmW1s;
         const int srow = MODE != 1 ? wbase + (int)crank * 64 : wbase + (int)crank * (BN / 2);
         const int srow2 = MODE != 1 ? srow + p.wup_off : srow + 64;
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(smem_u32(empty + stage), phase ^ 1);
-          const int nsub = min(KSUB, (p.kdim - kb * KST + BK - 1) / BK);   // skip all-OOB sub-tiles
-          const uint32_t fl = smem_u32(full + stage);
-          if (ti.swap) {
+        if (ti.swap) {
+          for (int kb = 0; kb * SWK * BK < p.kdim; ++kb) {
+            mbar_wait(smem_u32(empty + stage), phase ^ 1);
+            const int nsub = min(SWK, (p.kdim - kb * SWK * BK + BK - 1) / BK);
+            const uint32_t fl = smem_u32(full + stage);
             if (leader) mbar_expect_tx(fl, 2 * nsub * (BM * 128 + 32 * 128));
             const uint32_t fb = mapa_shared(fl, 0);
             for (int s2 = 0; s2 < nsub; ++s2) {
-              const uint32_t ad = smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128));
-              tma_load_2d_pair(ad, wms, fb, (kb * KSUB + s2) * BK, srow, ti.small ? pol_first : pol_last);
-              tma_load_2d_pair(ad + 64 * 128, wms, fb, (kb * KSUB + s2) * BK, srow2, ti.small ? pol_first : pol_last);
-              tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES + s2 * ((BN / 2) * 128)), &p.tmAs, fb,
-                               (kb * KSUB + s2) * BK, ti.row0 + (int)crank * 32, pol_act);
+              const uint32_t ad = s2 < 2 ? smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128))
+                                         : smem_u32(sB + stage * C::B_BYTES);
+              const uint32_t bd = smem_u32(sB + stage * C::B_BYTES + (SWK == 3 ? BM * 128 : 0) + s2 * (32 * 128));
+              tma_load_2d_pair(ad, wms, fb, (kb * SWK + s2) * BK, srow, ti.small ? pol_first : pol_last);
+              tma_load_2d_pair(ad + 64 * 128, wms, fb, (kb * SWK + s2) * BK, srow2, ti.small ? pol_first : pol_last);
+              tma_load_2d_pair(bd, &p.tmAs, fb, (kb * SWK + s2) * BK, ti.row0 + (int)crank * 32, pol_act);
             }
             if (++stage == S) {
               stage = 0;
               phase ^= 1;
             }
-            continue;
           }
+          continue;
+        }
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(smem_u32(empty + stage), phase ^ 1);
+          const int nsub = min(KSUB, (p.kdim - kb * KST + BK - 1) / BK);   // skip all-OOB sub-tiles
+          const uint32_t fl = smem_u32(full + stage);
           if (leader) mbar_expect_tx(fl, 2 * nsub * (C::STAGE / KSUB));
           const uint32_t fb = mapa_shared(fl, 0);
           for (int s2 = 0; s2 < nsub; ++s2) {
@@ -511,6 +524,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
         mbar_wait(smem_u32(tempty + acc), aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        if (ti.swap) {
+          for (int kb = 0; kb * SWK * BK < p.kdim; ++kb) {
+            mbar_wait(smem_u32(full + stage), phase);
+            tc_fence_after();
+            __syncwarp();
+            const int nsub = min(SWK, (p.kdim - kb * SWK * BK + BK - 1) / BK);
+#pragma unroll
+            for (int s2 = 0; s2 < SWK; ++s2) {
+              if (s2 < nsub) {
+                const uint64_t ad = smem_desc(s2 < 2 ? smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128))
+                                                     : smem_u32(sB + stage * C::B_BYTES));
+                const uint64_t bd = smem_desc(smem_u32(sB + stage * C::B_BYTES + (SWK == 3 ? BM * 128 : 0) +
+                                                       s2 * (32 * 128)));
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk)
+                  tc_mma_pair_w(d_tmem, ad + (uint32_t)((kk * 32) >> 4), bd + (uint32_t)((kk * 32) >> 4), idesc,
+                                (kb | s2 | kk) != 0);
+              }
+            }
+            tc_commit_pair_w(smem_u32(empty + stage));
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          tc_commit_pair_w(smem_u32(tfull + acc));
+          continue;
+        }
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(full + stage), phase);
           tc_fence_after();

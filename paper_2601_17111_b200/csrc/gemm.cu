@@ -1024,6 +1024,8 @@ struct BwdParams {
   void *out_foreign;     // KIND 1: output of foreign groups (wslot < 0), nullptr -> out[expert]
   float *ws;             // KIND 1: split-K partials
   int32_t num_sms;       // scheduling units for the split heuristic (SMs, or CTA pairs)
+  CUtensorMap tmAs;      // KIND 0 pair kernel, swapped tiles: activation rows, 32-row boxes
+  int32_t swap;          // KIND 0 pair kernel: groups of <= 64 rows as swapped tiles
   const __nv_bfloat16 *gu;   // KIND 2: [g | u] rows, gates, outputs w·a, [dg | du], partial dots
   const float *gate;
   __nv_bfloat16 *aw, *dgu;
@@ -1043,12 +1045,14 @@ __device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr) {
 struct BwdTile {
   int row0, row_end, m0, n0, g, nk, split, nsplit;
   int half;   // pair kernel, kind 0: <= 128 rows left in the block -> M=128 pair MMA
+  int swap;   // pair kernel, kind 0: <= 64 rows -> swapped tile D[features x tokens] (M=256, N=64)
 };
 
 template <int KIND>
 __device__ __forceinline__ BwdTile decode_bwd(int t, const BwdParams &p, const int *s_mblk) {
   BwdTile ti;
   ti.half = 0;
+  ti.swap = 0;
   if (KIND == 0) {
     const int mb = t / p.n_nt;
     ti.n0 = (t - mb * p.n_nt) * kBwdBN;
@@ -1344,6 +1348,7 @@ template <int KIND>
 __device__ __forceinline__ BwdTile decode_bwd_pair(int t, const BwdParams &p, const int *s_mblk) {
   BwdTile ti;
   ti.half = 0;
+  ti.swap = 0;
   if (KIND != 1) {
     const int mb = t / p.n_nt;
     ti.n0 = (t - mb * p.n_nt) * kBwdBN;
@@ -1360,6 +1365,7 @@ __device__ __forceinline__ BwdTile decode_bwd_pair(int t, const BwdParams &p, co
     ti.m0 = 0;
     ti.nk = (p.kdim + BK - 1) / BK;
     ti.half = ti.row_end - ti.row0 <= BM;
+    ti.swap = KIND == 0 && p.swap && ti.row_end - ti.row0 <= 64;
   } else {
     const int per = p.n_mt * p.n_nt;
     int lo = 0, hi = p.n_groups - 1;
@@ -1467,6 +1473,33 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
         const int ws = KIND != 1 ? p.groups[ti.g].wslot : 0;
         const int wrow = (ws >= 0 ? ws : -1 - ws) * p.kdim;
         const CUtensorMap *bm = (KIND != 1 && ws < 0) ? &p.tmB1 : &p.tmB;
+        if (KIND == 0 && ti.swap) {
+          // swapped tile, three 64-deep K sub-tiles per stage: this CTA's 128 weight features
+          // (MN-major, the M operand; sub-tiles 0/1 in the stage's B slots, 2 in its second A slot)
+          // and its 32 of the group's <= 64 token rows (K-major, the N operand; the first A slot)
+          for (int kq = 0; kq * 3 < ti.nk; ++kq) {
+            mbar_wait(smem_u32(empty + stage), phase ^ 1);
+            const int nsub = min(3, ti.nk - kq * 3);
+            const uint32_t fl = smem_u32(full + stage);
+            if (leader) mbar_expect_tx(fl, 2 * nsub * (kPairB + 32 * 128));
+            const uint32_t fb = mapa_shared(fl, 0);
+            for (int s2 = 0; s2 < nsub; ++s2) {
+              const int kb = kq * 3 + s2;
+              const uint32_t w_dst = s2 < 2 ? smem_u32(sB + (stage * KS + s2) * kPairB)
+                                            : smem_u32(sA + (stage * KS + 1) * kPairA);
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+                tma_load_2d_pair(w_dst + c * 8192, bm, fb, ti.n0 + (int)crank * 128 + c * 64, wrow + kb * BK, pol);
+              tma_load_2d_pair(smem_u32(sA + (stage * KS) * kPairA + s2 * (32 * 128)), &p.tmAs, fb, kb * BK,
+                               ti.row0 + (int)crank * 32, pol);
+            }
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          continue;
+        }
         for (int kq = 0; kq * KS < ti.nk; ++kq) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const int nsub = min(KS, ti.nk - kq * KS);
@@ -1513,6 +1546,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
         mbar_wait(smem_u32(tempty + acc), ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        if (KIND == 0 && ti.swap) {
+          // A = weights (MN-major), B = tokens (K-major), M=256, N=64
+          const uint32_t idesc_sw = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(64 >> 3) << 17) |
+                                    ((uint32_t)((2 * BM) >> 4) << 24);
+          for (int kq = 0; kq * 3 < ti.nk; ++kq) {
+            mbar_wait(smem_u32(full + stage), phase);
+            tc_fence_after();
+            const int nsub = min(3, ti.nk - kq * 3);
+            for (int s2 = 0; s2 < nsub; ++s2) {
+              const uint32_t w0 = s2 < 2 ? smem_u32(sB + (stage * KS + s2) * kPairB) : smem_u32(sA + (stage * KS + 1) * kPairA);
+              const uint32_t x0 = smem_u32(sA + (stage * KS) * kPairA + s2 * (32 * 128));
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk)
+                tc_mma_pair(d_tmem, smem_desc_mn(w0 + kk * 2048), smem_desc(x0 + kk * 32), idesc_sw,
+                            ((kq * 3 + s2) | kk) != 0);
+            }
+            tc_commit_pair(smem_u32(empty + stage));
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          tc_commit_pair(smem_u32(tfull + acc));
+          continue;
+        }
         for (int kq = 0; kq * KS < ti.nk; ++kq) {
           mbar_wait(smem_u32(full + stage), phase);
           tc_fence_after();
@@ -1633,6 +1691,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
           } else {
             dp[0] = dot;
             dp[1] = 0.f;
+          }
+        }
+      } else if (KIND == 0 && ti.swap) {
+        // swapped tile: TMEM lane = output column n0 + 128·crank + L, TMEM column j = token row0 + j
+        const int n = ti.n0 + (int)crank * 128 + q * 32 + lane;
+        __nv_bfloat16 *ocol = reinterpret_cast<__nv_bfloat16 *>(p.out) + n;
+#pragma unroll 1
+        for (int j = 0; j < 64; j += 8) {
+          float v[8];
+          tmem_ld8(taddr + j, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int row = ti.row0 + j + i;
+            if (n < p.nout && row < ti.row_end) ocol[(size_t)row * p.nout] = __float2bfloat16_rn(v[i]);
           }
         }
       } else if (KIND == 0) {
@@ -1838,6 +1911,10 @@ llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s) {
   p.out_foreign = a.out_foreign;
   p.ws = a.ws;
   p.num_sms = a.pair ? a.num_sms / 2 : a.num_sms;
+  {
+    const char *sw = getenv("LLEP_BWD_SWAP");   // A/B switch: swapped tiles in the row kind
+    p.swap = a.pair ? (sw ? atoi(sw) : 1) : 0;
+  }
   if (a.kind == 2) {
     if (!a.pair || !a.gu || !a.gate || !a.aw || !a.dgu || !a.dotp) {
       set_error("fused dA0 + SwiGLU-backward GEMM needs the pair kernel and all of gu, gate, aw, dgu, dotp");
@@ -1851,7 +1928,7 @@ llep_status run_gemm_bwd(const BwdArgs &a, cudaStream_t s) {
   }
   bool ok;
   if (a.kind != 1) {
-    ok = make_map_box(&p.tmA, a.a, a.rows, a.kdim, BK, BM) &&
+    ok = make_map_box(&p.tmA, a.a, a.rows, a.kdim, BK, BM) && make_map_box(&p.tmAs, a.a, a.rows, a.kdim, BK, 32) &&
          make_map_box(&p.tmB, a.b, (int64_t)a.n_weights * a.kdim, a.nout, 64, BK) &&
          make_map_box(&p.tmB1, a.b_foreign ? a.b_foreign : a.b,
                       (int64_t)(a.b_foreign ? a.n_foreign : a.n_weights) * a.kdim, a.nout, 64, BK);

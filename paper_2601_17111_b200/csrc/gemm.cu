@@ -12,8 +12,14 @@
 //     of W_up (two TMA boxes), so one accumulator tile holds both halves of each output column:
 //     A[r, n] = silu(acc[r, n]) * acc[r, BN/2 + n]   (no [n, 2H] intermediate in HBM)
 //   mode 1 (GEMM2 + gate): Y[r, n] = gate[r] * acc[r, n]   (Ĥ = Ĝ ⊙ B̂W)
+//   mode 2 (backward recompute): raw [g | u] rows;  mode 3 (training forward): mode 0 + mode 2 stores
 // Groups start at 128-aligned rows, so an M tile never straddles two experts; rows past a
 // group's end are computed on padding and masked at the store.
+// The default kernels are the CTA-pair versions (grouped_gemm_2cta_kernel, cta_group::2, groups
+// 256-row aligned): M=256 tiles, M=128 pair MMAs for blocks with <= 128 rows left, and SWAPPED tiles
+// for groups of <= 64 rows (D = W·Xᵀ: M=256 over weight rows, N=64 over the group's tokens, three
+// K sub-tiles per stage) -- at P=1 those are the cold experts, whose cost is streaming their weights.
+// Backward GEMMs (gemm_bwd_*_kernel, row f1) follow at the end of the file.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>

@@ -950,7 +950,10 @@ llep_status launch(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
   return LLEP_OK;
 }
 
-template <int BN, int MODE, int KSUB = 2>
+#ifndef LLEP_FWD_KSUB
+#define LLEP_FWD_KSUB 2   // forward pair GEMMs: 64-deep K sub-tiles per pipeline stage (A/B: 3)
+#endif
+template <int BN, int MODE, int KSUB = LLEP_FWD_KSUB>
 llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
   using C = Cfg2<BN, KSUB, (MODE == 0 || MODE == 3) ? kXchgBytes : kStoreStageBytes>;
   auto kern = grouped_gemm_2cta_kernel<BN, MODE, KSUB>;

@@ -307,3 +307,22 @@ def test_multiprocess_trace_replay_p2(L, tmp_path):
             mr, l2 = LC.errors(res[f"r{i}_llep"].astype(np.float64), ref)
             assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (p, i, mr, l2)
             assert bool(res[f"r{i}_same"])
+
+
+def test_peak_memory_bounded_by_plan(tmp_path):
+    """G120 at P=8 (8 processes on one GPU, each holding exactly one GPU's footprint), 95 %/1: every
+    rank's measured peak (torch allocations + the library context) stays within the §8(a) memory
+    model at the plan's own g_a[d] and |S_d| plus a fixed 0.6 GB slack (scratch), and every rank's
+    rows equal the capacity cap = B·K (the planner's constraint, α = 1)."""
+    import json
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, os.path.join(os.path.dirname(HERE), "tools", "mem_sweep.py"), "--config", "g120",
+           "--world", "8", "--scenarios", "95:1", "--modes", "llep", "--port", "29730"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    ll = line["llep"]
+    assert ll["transfers"] == 7 and not ll["fallback"]
+    assert ll["max_rows"] == W.CONFIGS["g120"].tokens_per_rank * W.CONFIGS["g120"].top_k
+    assert ll["peak_gb_per_gpu"] <= ll["model_gb_critical"] + 0.6, ll
+    assert ll["model_gb_critical"] < line["ep"]["model_gb_critical"] / 3

@@ -126,16 +126,20 @@ typedef struct {
 } llep_shape;
 
 /* Create the context for `rank` on CUDA device `device` (the caller's current device).
- * max_tokens: largest B this rank will pass.  Allocates the rank-local scratch and an initial
- * arena (grown by llep_context_reserve).  Errors: INVALID (shape rules above; D, H % 8 != 0;
- * P > 32), NOMEM, CUDA. */
+ * max_tokens: largest B any rank will pass -- the SAME value on every rank (the arenas are symmetric:
+ * peers address each other's regions with their own offsets; llep_context_open_peers compares every
+ * peer's arena geometry and fails with LLEP_ERR_INVALID if it differs).  Allocates the rank-local
+ * scratch and an initial arena (grown by llep_context_reserve).  Errors: INVALID (shape rules above;
+ * D, H % 8 != 0; P > 32), NOMEM, CUDA. */
 llep_status llep_context_create(const llep_shape *shape, int32_t rank, int32_t device,
                                 int64_t max_tokens, llep_context **out);
 void llep_context_destroy(llep_context *ctx);
 
 /* Symmetric-arena bootstrap.  Every rank calls get_handle, the caller all-gathers the P
  * 64-byte handles (any transport; the library needs only the bytes), and every rank calls
- * open_peers with the gathered [P][64] array.  P == 1 needs neither call. */
+ * open_peers with the gathered [P][64] array.  P == 1 needs neither call.  open_peers reads the
+ * geometry record at the start of every peer's arena and returns LLEP_ERR_INVALID when a peer's
+ * differs from this rank's (asymmetric max_tokens / reserve / backward setting). */
 llep_status llep_context_ipc_handle(llep_context *ctx, void *handle64);
 llep_status llep_context_open_peers(llep_context *ctx, const void *handles, int32_t n);
 
@@ -150,7 +154,8 @@ llep_status llep_context_reserve(llep_context *ctx, int64_t rows, int32_t foreig
  * like llep_context_reserve (re-exchange the IPC handles afterwards for P > 1). */
 llep_status llep_context_enable_backward(llep_context *ctx);
 
-/* Bytes the context currently holds on the device (arena + scratch). */
+/* Bytes the context currently holds on the device: arena, scratch, activations, backward buffers and
+ * the lazily grown backward workspaces (every cudaMalloc the context made). */
 int64_t llep_context_device_bytes(const llep_context *ctx);
 
 /* Per-GPU memory cap for the context's device allocations (0 = none).  A llep_context_reserve that
@@ -177,7 +182,8 @@ typedef struct {
  *   a4  planner kernel on C (λ test, LLA, LLAS, 𝒲) -> plan_out (device blob)
  *   a5  layout: per-device expert groups (native first, then foreign), 128-row aligned bases
  * then one device->host read of the requirements (needed to size the arena; the only host
- * synchronisation of the layer).
+ * synchronisation of the layer).  The context keeps the prepared ids (a device copy) and the
+ * topk_ids pointer: the following llep_moe_forward / backward must pass the same buffer unchanged.
  *   topk_ids   [B, K] int32, device.  Ids outside [0, N) -> LLEP_ERR_ROUTING.
  *   force_ep   1 -> standard EP plan on the same kernels (Alg. 1); 0 -> LLEP.
  *   plan_out   device buffer, llep_plan_bytes(N, P).
@@ -203,7 +209,14 @@ llep_status llep_prepare(llep_context *ctx, const int32_t *topk_ids, int64_t n_t
  *              and validated again (chunk totals == loads, else LLEP_ERR_PLAN); do not overwrite
  *              a prepared plan in place between llep_prepare and llep_moe_forward/backward
  *   out        [B, D] bf16, device
- * Errors: INVALID, PLAN (plan larger than the arena), CUDA, COMM. */
+ * The plan, load matrix and stable local ranks belong to the ids of the last llep_prepare, so:
+ *   - topk_ids must be the buffer passed to that llep_prepare (else LLEP_ERR_PLAN, immediately) and
+ *     B must equal its n_tokens (else LLEP_ERR_INVALID);
+ *   - if that buffer's contents changed since, the dispatch addresses every slot with the prepared
+ *     ids (every planned row is still written exactly once), drops the slots whose id changed from
+ *     the output and raises a sticky device flag reported as LLEP_ERR_PLAN by llep_context_check or
+ *     the next llep_prepare.
+ * Errors: INVALID, PLAN (plan larger than the arena; ids buffer not the prepared one), CUDA, COMM. */
 llep_status llep_moe_forward(llep_context *ctx, const uint16_t *x, const int32_t *topk_ids,
                              const float *topk_w, int64_t n_tokens, const uint16_t *w13,
                              const uint16_t *w2, const void *plan, uint16_t *out, void *stream);
@@ -277,6 +290,12 @@ typedef struct {
   int64_t gemm_rows;        /* Σ over timed calls of real rows this rank's GEMMs processed */
 } llep_stats;
 llep_status llep_context_set_timing(llep_context *ctx, int32_t enable);
+
+/* Synchronise `stream` and return (then clear) the sticky device-side error of the context's calls so
+ * far: LLEP_ERR_ROUTING (an id outside [0, N)), LLEP_ERR_COMM (a device barrier or weight-flag wait timed
+ * out, ~20 s), LLEP_ERR_PLAN (topk_ids changed between llep_prepare and llep_moe_forward/backward; those
+ * slots were dropped).  LLEP_OK if none.  The hot path itself never synchronises for these. */
+llep_status llep_context_check(llep_context *ctx, void *stream);
 /* Synchronises the pending events, writes the totals, resets them if `reset`. */
 llep_status llep_context_stats(llep_context *ctx, llep_stats *out, int32_t reset);
 

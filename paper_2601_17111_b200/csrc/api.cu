@@ -187,6 +187,7 @@ struct llep_context {
   // rank-local scratch
   int32_t *tile_cnt = nullptr, *tile_off = nullptr, *cnt = nullptr, *local_rank = nullptr;
   int32_t *slot_dst = nullptr, *err = nullptr, *lm_local = nullptr;
+  int32_t *prep_ids = nullptr;            // [max_tokens*K] the ids of the last llep_prepare
   int32_t *rows_on = nullptr, *chunk_row = nullptr, *foreign_slot = nullptr;
   int32_t *dev_padded = nullptr, *dev_foreign = nullptr;
   Group *groups = nullptr;
@@ -225,6 +226,8 @@ struct llep_context {
   std::vector<uint8_t> plan_host;
   const void *plan_dev_cached = nullptr;
   int64_t prepared_tokens = -1;
+  const int32_t *prepared_ids = nullptr;  // caller's topk_ids pointer of the last llep_prepare
+  size_t lazy_bytes = 0;                  // backward workspaces grown on demand (wsbuf, dotp)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // measurement
@@ -253,8 +256,21 @@ static void collect(llep_context *c) {
   c->pending = false;
 }
 
+// Geometry record at the start of every arena.  Peers address each other's regions with their OWN
+// offsets, so every rank's arena must have the same geometry; llep_context_open_peers reads each peer's
+// record through the peer mapping and refuses asymmetric arenas (different max_tokens, shape, reserve
+// or backward setting on some rank) instead of letting peer stores land at wrong addresses.
+struct ArenaGeometry {
+  int64_t arena_bytes, arena_rows, max_tokens;
+  int32_t arena_foreign, arena_grad, backward, N, K, D, H, P, row_align, magic;
+};
+constexpr int32_t kGeomMagic = 0x4c4c4550;   // "LLEP"
+constexpr size_t kGeomBytes = 256;
+
+static ArenaGeometry geometry(const llep_context *c);
+
 static void layout_offsets(llep_context *c, int64_t rows, int32_t foreign) {
-  size_t off = 0;
+  size_t off = kGeomBytes;
   c->off_flags = off;
   off += 4 * (kWeightFlag0 + kMaxGroups);
   c->off_lm = off;
@@ -281,7 +297,7 @@ static void layout_offsets(llep_context *c, int64_t rows, int32_t foreign) {
   c->off_grad = off;
   if (c->backward) off += (size_t)c->arena_grad * 3 * c->H * c->D * 4;
   off = (off + 1023) & ~size_t(1023);
-  c->off_slot = off;   // last: its size (this rank's max_tokens) may differ between ranks
+  c->off_slot = off;   // slot buffer [max_tokens*K, D] (max_tokens is identical on every rank)
   off += (size_t)std::max<int64_t>(c->max_tokens, 1) * c->K * c->D * 2;
   c->arena_bytes = (off + 4095) & ~size_t(4095);
 }
@@ -289,6 +305,28 @@ static void layout_offsets(llep_context *c, int64_t rows, int32_t foreign) {
 static size_t bwd_local_bytes(const llep_context *c, int64_t rows, int32_t foreign) {
   if (!c->backward) return 0;
   return (size_t)rows * c->H * 2 * 6 + (size_t)foreign * 3 * c->H * c->D * 4;
+}
+
+static ArenaGeometry geometry(const llep_context *c) {
+  ArenaGeometry g;
+  memset(&g, 0, sizeof(g));
+  g.arena_bytes = (int64_t)c->arena_bytes;
+  g.arena_rows = c->arena_rows;
+  g.max_tokens = c->max_tokens;
+  g.arena_foreign = c->arena_foreign;
+  g.arena_grad = c->arena_grad;
+  g.backward = c->backward ? 1 : 0;
+  g.N = c->N; g.K = c->K; g.D = c->D; g.H = c->H; g.P = c->P;
+  g.row_align = c->row_align;
+  g.magic = kGeomMagic;
+  return g;
+}
+
+// every device byte the context holds: arena + scratch + activations + backward buffers + lazily
+// grown backward workspaces
+static size_t held_bytes(const llep_context *c) {
+  return c->arena_bytes + c->scratch_bytes + (size_t)c->arena_rows * c->H * 2 +
+         bwd_local_bytes(c, c->arena_rows, c->arena_foreign) + c->lazy_bytes;
 }
 
 static void close_peers(llep_context *c) {
@@ -329,7 +367,7 @@ static llep_status alloc_arena(llep_context *c, int64_t rows, int32_t foreign) {
     probe_sizes.arena_grad = c->arena_grad;
     layout_offsets(&probe_sizes, rows, foreign);
     const int64_t need = (int64_t)(probe_sizes.arena_bytes + c->scratch_bytes + (size_t)rows * c->H * 2 +
-                                   bwd_local_bytes(c, rows, foreign));
+                                   bwd_local_bytes(c, rows, foreign) + c->lazy_bytes);
     if (need > c->mem_cap) {
       set_error("memory cap: the plan needs %.2f GB on this device (arena + activations + scratch), "
                 "cap %.2f GB", need / 1e9, c->mem_cap / 1e9);
@@ -348,7 +386,7 @@ static llep_status alloc_arena(llep_context *c, int64_t rows, int32_t foreign) {
   c->act = nullptr;
   layout_offsets(c, rows, foreign);
   LLEP_CUDA(cudaMalloc(&c->arena, c->arena_bytes));
-  LLEP_CUDA(cudaMemset(c->arena, 0, c->off_x));  // flags + load matrix
+  LLEP_CUDA(cudaMemset(c->arena, 0, c->off_x));  // geometry + flags + load matrix
   LLEP_CUDA(cudaMalloc(&c->act, (size_t)rows * c->H * 2));
   if (c->backward) {
     LLEP_CUDA(cudaMalloc(&c->gu, (size_t)rows * 2 * c->H * 2));
@@ -360,6 +398,10 @@ static llep_status alloc_arena(llep_context *c, int64_t rows, int32_t foreign) {
   }
   c->arena_rows = rows;
   c->arena_foreign = foreign;
+  {
+    const ArenaGeometry g = geometry(c);
+    LLEP_CUDA(cudaMemcpy(c->arena, &g, sizeof(g), cudaMemcpyHostToDevice));
+  }
   c->peer_base[c->rank] = c->arena;
   if (c->P == 1) {
     c->peers_ready = true;
@@ -454,6 +496,7 @@ llep_status llep_context_create(const llep_shape *s, int32_t rank, int32_t devic
   if (!e) e = A(&c->tile_off, sizeof(int32_t) * tiles * N);
   if (!e) e = A(&c->cnt, sizeof(int32_t) * N);
   if (!e) e = A(&c->local_rank, sizeof(int32_t) * slots);
+  if (!e) e = A(&c->prep_ids, sizeof(int32_t) * slots);
   if (!e) e = A(&c->slot_dst, sizeof(int32_t) * 2 * slots);
   if (!e) e = A(&c->err, sizeof(int32_t) * 4);
   if (!e) e = A(&c->lm_local, sizeof(int32_t) * P * N);
@@ -495,7 +538,7 @@ void llep_context_destroy(llep_context *c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   close_peers(c);
-  void *ptrs[] = {c->tile_cnt, c->tile_off, c->cnt, c->local_rank, c->slot_dst, c->err,
+  void *ptrs[] = {c->tile_cnt, c->tile_off, c->cnt, c->local_rank, c->prep_ids, c->slot_dst, c->err,
                   c->lm_local, c->rows_on, c->chunk_row, c->foreign_slot, c->dev_padded,
                   c->dev_foreign, c->groups, c->sched, c->summary, c->d_ptrs, c->act, c->arena,
                   c->gu, c->da0, c->aw, c->dgu, c->stage13, c->stage2, c->wsbuf, c->dotp};
@@ -542,6 +585,25 @@ llep_status llep_context_open_peers(llep_context *c, const void *handles, int32_
     c->peer_base[q] = reinterpret_cast<uint8_t *>(p);
     c->peer_opened[q] = true;
   }
+  const ArenaGeometry mine = geometry(c);
+  for (int q = 0; q < c->P; ++q) {
+    ArenaGeometry g;
+    cudaError_t e = cudaMemcpy(&g, c->peer_base[q], sizeof(g), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      close_peers(c);
+      return cuda_status(e, "reading a peer's arena geometry");
+    }
+    if (memcmp(&g, &mine, sizeof(g)) != 0) {
+      set_error("asymmetric arenas: rank %d has max_tokens %lld, rows %lld, foreign %d, grad %d, backward %d; "
+                "rank %d has %lld, %lld, %d, %d, %d (every rank must create its context with the same shape and "
+                "max_tokens and call llep_context_reserve / enable_backward with the same arguments)",
+                q, (long long)g.max_tokens, (long long)g.arena_rows, g.arena_foreign, g.arena_grad, g.backward,
+                c->rank, (long long)mine.max_tokens, (long long)mine.arena_rows, mine.arena_foreign,
+                mine.arena_grad, mine.backward);
+      close_peers(c);
+      return LLEP_ERR_INVALID;
+    }
+  }
   c->peers_ready = true;
   return upload_peer_ptrs(c);
 }
@@ -578,7 +640,7 @@ llep_status llep_context_set_memory_cap(llep_context *c, int64_t bytes) {
 
 int64_t llep_context_device_bytes(const llep_context *c) {
   if (!c) return 0;
-  return (int64_t)(c->arena_bytes + c->scratch_bytes + (size_t)c->arena_rows * c->H * 2);
+  return (int64_t)held_bytes(c);
 }
 
 static uint32_t *const *peer_flags(llep_context *c) { return reinterpret_cast<uint32_t *const *>(c->d_ptrs); }
@@ -645,6 +707,25 @@ static llep_status run_layout(llep_context *c, const void *plan, cudaStream_t s)
   return LLEP_OK;
 }
 
+// Sticky device error words (err[4]): [0] a router index outside [0, N) (a1); [1] a device barrier (4),
+// weight-flag wait (8) or GEMM weight wait (16) timed out; [2] topk_ids changed between llep_prepare and
+// the forward / backward call (those slots were dropped).  Reported once, then cleared.
+static llep_status decode_err(llep_context *c, const int32_t *e, cudaStream_t s) {
+  if (!(e[0] | e[1] | e[2])) return LLEP_OK;
+  cudaMemsetAsync(c->err, 0, sizeof(int32_t) * 4, s);
+  if (e[0]) {
+    set_error("router index outside [0, N)");
+    return LLEP_ERR_ROUTING;
+  }
+  if (e[1]) {
+    set_error("device barrier or weight-flag wait timed out (a peer did not arrive), code %d", e[1]);
+    return LLEP_ERR_COMM;
+  }
+  set_error("topk_ids changed between llep_prepare and llep_moe_forward/backward: the changed slots were "
+            "dropped from that call's output");
+  return LLEP_ERR_PLAN;
+}
+
 // one host synchronisation: plan blob + layout summary + error flags
 static llep_status read_back(llep_context *c, const void *plan, cudaStream_t s) {
   const size_t pb = plan_layout(c->N, c->P).bytes;
@@ -658,15 +739,8 @@ static llep_status read_back(llep_context *c, const void *plan, cudaStream_t s) 
   LLEP_CUDA(cudaStreamSynchronize(s));
   c->plan_host.assign(c->plan_mirror, c->plan_mirror + pb);
   c->plan_dev_cached = plan;
-  if (c->err_host[0]) {
-    cudaMemsetAsync(c->err, 0, sizeof(int32_t) * 4, s);
-    set_error("router index outside [0, N)");
-    return LLEP_ERR_ROUTING;
-  }
-  if (c->err_host[1]) {
-    set_error("device barrier timed out (a peer did not arrive)");
-    return LLEP_ERR_COMM;
-  }
+  llep_status st = decode_err(c, c->err_host, s);
+  if (st != LLEP_OK) return st;
   if (c->summary_host->error) {
     set_error("plan inconsistent with the load matrix (chunk totals != l_e) or too many groups");
     return LLEP_ERR_PLAN;
@@ -687,6 +761,8 @@ llep_status llep_prepare(llep_context *c, const int32_t *ids, int64_t B, const l
   cudaStream_t s = (cudaStream_t)stream;
   collect(c);
   c->pending = false;
+  c->prepared_tokens = -1;   // a failed prepare leaves nothing for llep_moe_forward to use
+  c->prepared_ids = nullptr;
   const int N = c->N, P = c->P;
   const int64_t slots = B * c->K;
   const int n_tiles = (int)((slots + kTileSlots - 1) / kTileSlots);
@@ -699,7 +775,7 @@ llep_status llep_prepare(llep_context *c, const int32_t *ids, int64_t B, const l
   } else {
     LLEP_CUDA(cudaMemsetAsync(c->cnt, 0, sizeof(int32_t) * N, s));
   }
-  LLEP_CUDA(launch_local_rank(ids, slots, N, c->tile_off, c->local_rank, s));
+  LLEP_CUDA(launch_local_rank(ids, slots, N, c->tile_off, c->local_rank, c->prep_ids, s));
   mark(c, 1, s);
   // a2: push the counts row into every rank's load matrix, barrier, keep a local copy
   LLEP_CUDA(launch_push_counts(c->cnt, N, c->rank, P, peer_lm(c), s));
@@ -716,6 +792,7 @@ llep_status llep_prepare(llep_context *c, const int32_t *ids, int64_t B, const l
   mark(c, 3, s);
   if ((st = read_back(c, plan_out, s)) != LLEP_OK) return st;
   c->prepared_tokens = B;
+  c->prepared_ids = ids;
   if (req) fill_req(c, req);
   return LLEP_OK;
 }
@@ -792,6 +869,11 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   if (!c || !plan || !w13 || !w2 || (B > 0 && (!x || !ids || !topk_w || !out)))
     return invalid("null pointer");
   if (B != c->prepared_tokens) return invalid("n_tokens differs from the last llep_prepare");
+  if (B > 0 && ids != c->prepared_ids) {
+    set_error("topk_ids is not the buffer passed to the last llep_prepare (the plan, load matrix and local "
+              "ranks were computed from that one)");
+    return LLEP_ERR_PLAN;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   llep_status st;
   if (plan != c->plan_dev_cached) {
@@ -825,6 +907,8 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   da.ids = ids;
   da.w = topk_w;
   da.local_rank = c->local_rank;
+  da.prep_ids = c->prep_ids;
+  da.err = c->err;
   da.load_matrix = c->lm_local;
   da.plan = plan;
   da.chunk_row = c->chunk_row;
@@ -866,6 +950,7 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   g1.out = c->act;
   g1.wflags = P > 1 ? reinterpret_cast<const uint32_t *>(c->arena + c->off_flags) + kWeightFlag0 : nullptr;
   g1.wepoch = wepoch;
+  g1.err = c->err;
   g1.row_src = nullptr;
   g1.peer_slot = nullptr;
   g1.num_sms = c->num_sms;
@@ -920,6 +1005,26 @@ llep_status llep_moe_forward_train(llep_context *c, const uint16_t *x, const int
   return moe_forward(c, x, ids, topk_w, B, w13, w2, plan, out, gu_save, gu_rows, stream);
 }
 
+// Grow a lazily sized backward workspace (floats), counted in llep_context_device_bytes and checked
+// against the memory cap like the arena.
+static llep_status grow_lazy(llep_context *c, float **buf, int64_t *cap, int64_t need, cudaStream_t s) {
+  const size_t add = (size_t)(need - *cap) * 4;
+  if (c->mem_cap > 0 && (int64_t)(held_bytes(c) + add) > c->mem_cap) {
+    set_error("memory cap: the backward workspace needs %.2f GB more on this device, cap %.2f GB", add / 1e9,
+              c->mem_cap / 1e9);
+    return LLEP_ERR_NOMEM;
+  }
+  LLEP_CUDA(cudaStreamSynchronize(s));
+  if (*buf) cudaFree(*buf);
+  c->lazy_bytes -= (size_t)*cap * 4;
+  *buf = nullptr;
+  *cap = 0;
+  LLEP_CUDA(cudaMalloc(buf, (size_t)need * 4));
+  *cap = need;
+  c->lazy_bytes += (size_t)need * 4;
+  return LLEP_OK;
+}
+
 // This rank's expert groups in the layout kernel's order (native with rows, then foreign, ascending
 // ids), from the host copy of the plan: rows, weight slot (>= 0 native, -1-f foreign), expert.
 static void my_groups_host(const llep_context *c, std::vector<int32_t> &rows, std::vector<int32_t> &wslot,
@@ -958,6 +1063,11 @@ static llep_status moe_backward(llep_context *c, const uint16_t *x, const int32_
     return invalid("null pointer");
   if (!c->backward) return invalid("call llep_context_enable_backward first");
   if (B != c->prepared_tokens) return invalid("n_tokens differs from the last llep_prepare");
+  if (B > 0 && ids != c->prepared_ids) {
+    set_error("topk_ids is not the buffer passed to the last llep_prepare (the plan, load matrix and local "
+              "ranks were computed from that one)");
+    return LLEP_ERR_PLAN;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   llep_status st;
   if (plan != c->plan_dev_cached) {
@@ -995,6 +1105,8 @@ static llep_status moe_backward(llep_context *c, const uint16_t *x, const int32_
   da.ids = ids;
   da.w = topk_w;
   da.local_rank = c->local_rank;
+  da.prep_ids = c->prep_ids;
+  da.err = c->err;
   da.load_matrix = c->lm_local;
   da.plan = plan;
   da.chunk_row = c->chunk_row;
@@ -1082,12 +1194,7 @@ static llep_status moe_backward(llep_context *c, const uint16_t *x, const int32_
       const int nparts = 2 * ((H + 255) / 256);
       const int64_t need = c->arena_rows * nparts;
       if (need > c->dotp_cap) {
-        LLEP_CUDA(cudaStreamSynchronize(s));
-        if (c->dotp) cudaFree(c->dotp);
-        c->dotp = nullptr;
-        c->dotp_cap = 0;
-        LLEP_CUDA(cudaMalloc(&c->dotp, (size_t)need * 4));
-        c->dotp_cap = need;
+        if ((st = grow_lazy(c, &c->dotp, &c->dotp_cap, need, s)) != LLEP_OK) return st;
       }
       b.kind = 2;
       b.gu = GU;
@@ -1117,12 +1224,7 @@ static llep_status moe_backward(llep_context *c, const uint16_t *x, const int32_
     const int64_t need_ws = std::max(wgrad_workspace(grows.data(), (int)grows.size(), D, H, units),
                                      wgrad_workspace(grows.data(), (int)grows.size(), 2 * H, D, units));
     if (need_ws > c->ws_cap) {
-      LLEP_CUDA(cudaStreamSynchronize(s));
-      if (c->wsbuf) cudaFree(c->wsbuf);
-      c->wsbuf = nullptr;
-      c->ws_cap = 0;
-      LLEP_CUDA(cudaMalloc(&c->wsbuf, (size_t)need_ws * 4));
-      c->ws_cap = need_ws;
+      if ((st = grow_lazy(c, &c->wsbuf, &c->ws_cap, need_ws, s)) != LLEP_OK) return st;
     }
     BwdArgs w;
     memset(&w, 0, sizeof(w));
@@ -1243,6 +1345,17 @@ llep_status llep_moe_backward_saved(llep_context *c, const uint16_t *x, const in
   if (!gu_saved) return invalid("null pointer (gu_saved)");
   return moe_backward(c, x, ids, topk_w, dout, B, w13, w2, plan, dx, dgates, dw13, dw2, gu_saved, gu_rows,
                       stream);
+}
+
+llep_status llep_context_check(llep_context *c, void *stream) {
+  if (!c) return invalid("null context");
+  cudaStream_t s = (cudaStream_t)stream;
+  LLEP_CUDA(cudaStreamSynchronize(s));
+  int32_t e[4];
+  LLEP_CUDA(cudaMemcpy(e, c->err, sizeof(e), cudaMemcpyDeviceToHost));
+  llep_status st = decode_err(c, e, s);
+  LLEP_CUDA(cudaStreamSynchronize(s));
+  return st;
 }
 
 llep_status llep_context_set_timing(llep_context *c, int32_t enable) {

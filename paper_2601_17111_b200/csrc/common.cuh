@@ -129,7 +129,7 @@ cudaError_t launch_tile_count(const int32_t *ids, int64_t n_slots, int32_t N, in
 cudaError_t launch_tile_scan(const int32_t *tile_cnt, int32_t n_tiles, int32_t N, int32_t *tile_off,
                              int32_t *cnt_out, cudaStream_t s);
 cudaError_t launch_local_rank(const int32_t *ids, int64_t n_slots, int32_t N, const int32_t *tile_off,
-                              int32_t *local_rank, cudaStream_t s);
+                              int32_t *local_rank, int32_t *prep_ids, cudaStream_t s);
 cudaError_t launch_push_counts(const int32_t *cnt, int32_t N, int32_t rank, int32_t P,
                                int32_t *const *peer_lm, cudaStream_t s);
 cudaError_t launch_barrier(uint32_t *const *peer_flags, int32_t rank, int32_t P, uint32_t epoch,
@@ -160,6 +160,8 @@ struct DispatchArgs {
   const int32_t *ids;       // [B, K]
   const float *w;           // [B, K]
   const int32_t *local_rank;
+  const int32_t *prep_ids;  // [B, K] the ids llep_prepare planned with (addressing uses these)
+  int32_t *err;             // err[2] |= 1: a slot's id differs from the prepared one (slot dropped)
   const int32_t *load_matrix;
   const void *plan;
   const int32_t *chunk_row;
@@ -205,6 +207,8 @@ struct GemmArgs {
   uint16_t *out2;            // mode 3 (GEMM1 + SwiGLU that also saves [g | u]): [rows, 2*nout]
   const uint32_t *wflags;    // row f2: foreign slot f's weights landed when wflags[f] >= wepoch
   uint32_t wepoch;           //         (nullptr: weights already resident)
+  int32_t *err;              //         err[1] |= 16 if a weight wait times out (~20 s); waits are
+                             //         skipped once err[1] is set (a peer failed: no hang)
   const int32_t *row_src;    // mode 1 push epilogue: (slot << 5) | rank of each receive row, and
   uint16_t *const *peer_slot;//   [P] slot buffers [B*K, nout]: the row's output goes to
                              //   peer_slot[rank] + slot*nout (nullptr: write `out` rows)

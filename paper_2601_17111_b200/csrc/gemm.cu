@@ -60,6 +60,7 @@ struct GemmParams {
   __nv_bfloat16 *out;
   const uint32_t *wflags;
   uint32_t wepoch;
+  int32_t *err;
   const int32_t *row_src;
   uint16_t *const *peer_slot;
   __nv_bfloat16 *out2;   // mode 3: raw [g | u] pre-activations, rows of 2 * nout (training forward)
@@ -67,13 +68,26 @@ struct GemmParams {
 
 // Row f2: wait until foreign slot f's weights have landed (flag published by the native device
 // with release semantics after its copy-engine push), then order the TMA reads after it.
+// Bounded like the device barriers: after ~20 s (or once another wait / barrier of this rank has
+// failed, err[1] != 0) it gives up and flags err[1] |= 16 (LLEP_ERR_COMM at the next check), so a peer
+// that returned early cannot hang this GPU.
 __device__ __forceinline__ void wait_weights(const GemmParams &p, int wslot) {
   if (wslot >= 0 || !p.wflags) return;
   const uint32_t *f = p.wflags + (-1 - wslot);
   uint32_t v;
-  do {
+  const long long t0 = clock64();
+  long long spins = 0;
+  while (true) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-  } while ((int32_t)(v - p.wepoch) < 0);
+    if ((int32_t)(v - p.wepoch) >= 0) break;
+    if (((++spins) & 255) == 0) {
+      if (p.err && *reinterpret_cast<volatile int32_t *>(p.err + 1) != 0) break;
+      if (clock64() - t0 > 40000000000LL) {
+        if (p.err) atomicOr(p.err + 1, 16);
+        break;
+      }
+    }
+  }
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
@@ -2011,6 +2025,7 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   prm.sched = g.sched;
   prm.wflags = g.wflags;
   prm.wepoch = g.wepoch;
+  prm.err = g.err;
   prm.row_src = g.row_src;
   prm.peer_slot = g.peer_slot;
   prm.n_groups_dev = g.n_groups_dev;

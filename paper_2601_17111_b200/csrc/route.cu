@@ -80,7 +80,7 @@ constexpr int kSlotsPerWarp = kTileSlots / kRankWarps;
 
 __global__ void __launch_bounds__(kRankThreads) local_rank_kernel(
     const int32_t *__restrict__ ids, int64_t n_slots, int N, const int32_t *__restrict__ tile_off,
-    int32_t *__restrict__ local_rank) {
+    int32_t *__restrict__ local_rank, int32_t *__restrict__ prep_ids) {
   extern __shared__ int32_t wcnt[];  // [kRankWarps][N]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kRankWarps * N; i += kRankThreads) wcnt[i] = 0;
@@ -114,7 +114,10 @@ __global__ void __launch_bounds__(kRankThreads) local_rank_kernel(
     int base = 0;
     if (e >= 0) base = mine[e];
     __syncwarp();
-    if (j < n_slots) local_rank[j] = e >= 0 ? base + r : -1;
+    if (j < n_slots) {
+      local_rank[j] = e >= 0 ? base + r : -1;
+      prep_ids[j] = e;   // the ids this plan was built from: dispatch addresses with these (a5)
+    }
     if (e >= 0 && lane == __ffs(peers) - 1) mine[e] = base + __popc(peers);
     __syncwarp();
   }
@@ -177,7 +180,12 @@ __global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_kernel(DispatchA
   int dev = -1, row = 0;
   if (lane < K) {
     const int64_t j = t * K + lane;
-    const int e = a.ids[j];
+    // The plan, the load matrix and the local ranks all come from llep_prepare's ids, so the slot is
+    // addressed with those (every planned receive row is written exactly once); a slot whose id
+    // changed since then is dropped from the combine and reported (err[2], LLEP_ERR_PLAN).
+    const int e = a.prep_ids[j];
+    const bool changed = a.ids[j] != e;
+    if (changed) atomicOr(a.err + 2, 1);
     if (e >= 0 && e < N) {
       int g = a.local_rank[j];
       for (int q = 0; q < a.rank; ++q) g += a.load_matrix[(size_t)q * N + e];  // rank-major (R11)
@@ -191,10 +199,10 @@ __global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_kernel(DispatchA
         }
       }
     }
-    a.slot_dst[2 * j] = dev;
+    a.slot_dst[2 * j] = changed ? -1 : dev;
     a.slot_dst[2 * j + 1] = row;
     if (dev >= 0) {
-      a.peer_g[dev][row] = a.w[j];
+      a.peer_g[dev][row] = changed ? 0.f : a.w[j];
       // (source rank, flat slot) of this receive row: the GEMM2 epilogue pushes the row's output
       // straight into slot j of this rank's slot buffer
       if (a.peer_rsrc) a.peer_rsrc[dev][row] = (int32_t)((j << 5) | a.rank);
@@ -577,7 +585,7 @@ cudaError_t launch_tile_scan(const int32_t *tile_cnt, int32_t n_tiles, int32_t N
 }
 
 cudaError_t launch_local_rank(const int32_t *ids, int64_t n_slots, int32_t N, const int32_t *tile_off,
-                              int32_t *local_rank, cudaStream_t s) {
+                              int32_t *local_rank, int32_t *prep_ids, cudaStream_t s) {
   const int n_tiles = (int)((n_slots + kTileSlots - 1) / kTileSlots);
   if (n_tiles == 0) return cudaSuccess;
   const size_t smem = sizeof(int32_t) * kRankWarps * N;
@@ -586,7 +594,7 @@ cudaError_t launch_local_rank(const int32_t *ids, int64_t n_slots, int32_t N, co
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  local_rank_kernel<<<n_tiles, kRankThreads, smem, s>>>(ids, n_slots, N, tile_off, local_rank);
+  local_rank_kernel<<<n_tiles, kRankThreads, smem, s>>>(ids, n_slots, N, tile_off, local_rank, prep_ids);
   return cudaGetLastError();
 }
 

@@ -80,6 +80,7 @@ _SIGS = {
                                                _vp, _vp, _vp]),
     "llep_debug_copy": (ctypes.c_int, [_vp, _i32, _vp, _i64, _vp]),
     "llep_context_set_timing": (ctypes.c_int, [_vp, _i32]),
+    "llep_context_check": (ctypes.c_int, [_vp, _vp]),
     "llep_context_stats": (ctypes.c_int, [_vp, ctypes.c_void_p, _i32]),
     "llep_gemm_bwd": (ctypes.c_int, [_i32, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
     "llep_grouped_gemm": (ctypes.c_int, [_i32, _vp, _i64, _i32, _vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
@@ -179,6 +180,13 @@ def plan_device(load_matrix, world: int, alpha: float = 1.0, min_chunk: int = 10
 
 
 # ------------------------------------------------------------------------------ context
+def _max_over_group(v: int, group) -> int:
+    import torch.distributed as dist
+    allv: list = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allv, v, group=group)
+    return max(allv)
+
+
 class Context:
     """One rank's LLEP context: scratch, symmetric arena, peer mappings."""
 
@@ -190,6 +198,8 @@ class Context:
         self.M = n_experts // world
         self.device = device
         self.group = group
+        if world > 1:   # the arenas must be symmetric: every rank sizes its context for the largest B
+            max_tokens = _max_over_group(int(max_tokens), group)
         self.max_tokens = max_tokens
         h = _vp()
         torch.cuda.set_device(device)
@@ -231,6 +241,10 @@ class Context:
         _check(_lib.llep_context_enable_backward(self._h))
         if self.P > 1:
             self.exchange_handles()
+
+    def check(self) -> None:
+        """llep_context_check: synchronise and raise the sticky device-side error, if any."""
+        _check(_lib.llep_context_check(self._h, _stream_ptr()))
 
     def set_timing(self, on: bool = True) -> None:
         _check(_lib.llep_context_set_timing(self._h, int(on)))

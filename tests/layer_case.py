@@ -58,3 +58,72 @@ def oracle_rank_output(shape: W.LayerShape, rank: int, ids: np.ndarray, gates: n
 def errors(y: np.ndarray, r: np.ndarray):
     from oracle import layer as O3
     return O3.relative_errors(y, r)
+
+
+def expected_layout(plan, d: int, row_align: int = 256):
+    """Device d's group table as rows a5 of SURVEY §8 define it, derived here from the oracle plan:
+    native experts of d with rows on d (ascending id), then the foreign experts S_d (ascending id); each
+    group holds e's chunks on d concatenated in plan order and starts at the running sum of the earlier
+    groups' row counts rounded up to `row_align` (the GEMM's M tile).  -> [(expert, wslot, base, n)]"""
+    from oracle import schedule as O2
+    M = plan.experts_per_device
+    out, base, f = [], 0, 0
+    for native in (True, False):
+        for e in range(plan.n_experts):
+            if (e // M == d) != native:
+                continue
+            n = O2.rows_on_device(plan, e, d)
+            if n == 0:
+                continue
+            out.append((e, e - d * M if native else -1 - f, base, n))
+            f += 0 if native else 1
+            base += -(-n // row_align) * row_align
+    return out
+
+
+def check_index_work(res, key: str, plan, ids_all, n_experts: int):
+    """Rows a1-a5 bit-exact against O2 on every rank (north star: integer / index work bit-exact):
+    the all-gathered load matrix C, every slot's stable local rank r_j, every device's group table,
+    and every slot's destination (device, row) = (d_j, base_d[e_j] + pos_j) with (d_j, pos_j) from
+    O2.slot_destinations (rank-major global index R11, chunk lookup P:547-548)."""
+    from oracle import schedule as O2
+    P = len(ids_all)
+    C = O2.load_matrix(ids_all, n_experts)
+    base = []
+    for d in range(P):
+        lay = expected_layout(plan, d)
+        g = res[d][f"{key}_groups"]
+        got = [tuple(int(v) for v in row[:4]) for row in g]
+        assert got == lay, (key, d, got[:4], lay[:4])
+        base.append({e: b for (e, _w, b, _n) in lay})
+    for p in range(P):
+        assert np.array_equal(res[p][f"{key}_lm"], C), (key, p)
+        assert np.array_equal(res[p][f"{key}_lr"], O2.local_rank_in_expert(ids_all[p])), (key, p)
+        dev, pos = O2.slot_destinations(plan, C, ids_all[p], p)
+        flat = ids_all[p].reshape(-1)
+        row = np.array([base[d][int(e)] for d, e in zip(dev, flat)], dtype=np.int64) + pos
+        dst = res[p][f"{key}_dst"]
+        assert np.array_equal(dst[:, 0], dev), (key, p)
+        assert np.array_equal(dst[:, 1], row), (key, p)
+
+
+def boundary_tokens(plan, ids_all, n_experts: int, extra: int = 16):
+    """Per rank, the tokens whose slots sit at the first and last global index of every plan chunk (so
+    every chunk and group boundary on every device is sampled), plus each rank's first `extra` tokens.
+    -> {rank: sorted token indices}."""
+    from oracle import schedule as O2
+    P = len(ids_all)
+    C = O2.load_matrix(ids_all, n_experts)
+    K = ids_all[0].shape[1]
+    gidx = [O2.global_index(ids_all[p], C, p) for p in range(P)]
+    flat = [ids_all[p].reshape(-1) for p in range(P)]
+    want = {p: set(range(min(extra, ids_all[p].shape[0]))) for p in range(P)}
+    for e, A in enumerate(plan.chunks):
+        for (_d, s, t) in A:
+            for g in (s, t - 1):
+                for p in range(P):
+                    hit = np.nonzero((flat[p] == e) & (gidx[p] == g))[0]
+                    if hit.size:
+                        want[p].add(int(hit[0]) // K)
+                        break
+    return {p: np.array(sorted(v), dtype=np.int64) for p, v in want.items()}

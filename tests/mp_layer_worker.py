@@ -4,8 +4,11 @@
 
 The ranks bootstrap a gloo process group on 127.0.0.1 (plumbing only: it carries the 64-byte CUDA
 IPC handles); all data moves through the library's peer-mapped arenas and device barriers.
-Each rank writes OUTDIR/rank{p}.npz with its LLEP output, EP output (the first SAMPLE rows if given),
-the plan blob and whether the whole LLEP and EP outputs are bitwise equal."""
+Each rank writes OUTDIR/rank{p}.npz with its LLEP output, EP output (the first SAMPLE rows if given, or
+the rows listed under key r{p} of the .npz file named by LLEP_TEST_ROWS), the plan blob, whether the
+whole LLEP and EP outputs are bitwise equal, and the index work of both calls (load matrix, stable
+local ranks, per-slot (device, row) destinations and this rank's group table) for bit-exact comparison
+with the oracle O2."""
 import os
 import sys
 
@@ -14,6 +17,18 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
 sys.path.insert(0, HERE)
+
+
+def dump_index_work(L, ctx, sh, P, key):
+    """The index work of the last prepare + forward (rows a1-a5): C [P, N], r_j [B*K], (dev, row) [B*K, 2]
+    and this rank's group table [G, 8] = (expert, weight slot, row_base, n_rows, mblk_start, 0, 0, 0)."""
+    import torch
+    BK = sh.tokens_per_rank * sh.top_k
+    G = int(ctx.last_req.my_groups)
+    return {f"{key}_lm": ctx.debug(L.DBG_LOAD_MATRIX, P * sh.n_experts, torch.int32).cpu().numpy().reshape(P, -1),
+            f"{key}_lr": ctx.debug(L.DBG_LOCAL_RANK, BK, torch.int32).cpu().numpy(),
+            f"{key}_dst": ctx.debug(L.DBG_SLOT_DST, 2 * BK, torch.int32).cpu().numpy().reshape(-1, 2),
+            f"{key}_groups": ctx.debug(L.DBG_GROUPS, 8 * G, torch.int32).cpu().numpy().reshape(G, 8)}
 
 
 def worker(rank, P, cfg, pct, nhot, outdir, sample):
@@ -58,11 +73,17 @@ def worker(rank, P, cfg, pct, nhot, outdir, sample):
     plan = ctx.prepare(ids, alpha, m, lam)[0]          # plan of the LLEP call (deterministic)
     plan_np = plan.cpu().numpy()
     out_llep2 = ctx.forward(x, ids, gates, w13, w2, plan)   # second iteration on the same arena
+    index_work = dump_index_work(L, ctx, sh, P, "llep")
     out_ep = ctx(x, ids, gates, w13, w2, ep=True)
+    index_work.update(dump_index_work(L, ctx, sh, P, "ep"))
     torch.cuda.synchronize()
     assert torch.equal(out_llep, out_llep2), "iteration-to-iteration mismatch"
     n = sample if sample > 0 else out_llep.shape[0]
-    extra = {}
+    rows_file = os.environ.get("LLEP_TEST_ROWS")
+    sel = slice(0, n)
+    if rows_file:
+        sel = torch.from_numpy(np.load(rows_file)[f"r{rank}"].astype(np.int64)).to(out_llep.device)
+    extra = dict(index_work)
     if os.environ.get("LLEP_TEST_BWD") == "1":
         ctx.enable_backward()
         dout = W.tokens_torch(sh.tokens_per_rank, sh.d_model, rank + 1000, f"cuda:{dev}", 21)
@@ -75,10 +96,10 @@ def worker(rank, P, cfg, pct, nhot, outdir, sample):
         torch.cuda.synchronize()
         for a_, b_ in zip(saved, (dx, dg, dw13, dw2)):
             assert torch.equal(a_, b_), "saved-preactivation backward differs from the recompute"
-        extra = dict(dx=dx[:n].float().cpu().numpy(), dgates=dg[:n].cpu().numpy(), dw13=dw13.cpu().numpy(),
+        extra.update(dx=dx[sel].float().cpu().numpy(), dgates=dg[sel].cpu().numpy(), dw13=dw13.cpu().numpy(),
                      dw2=dw2.cpu().numpy())
-    np.savez(os.path.join(outdir, f"rank{rank}.npz"), llep=out_llep[:n].float().cpu().numpy(),
-             ep=out_ep[:n].float().cpu().numpy(), plan=plan_np,
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), llep=out_llep[sel].float().cpu().numpy(),
+             ep=out_ep[sel].float().cpu().numpy(), plan=plan_np,
              same=np.array(bool(torch.equal(out_llep, out_ep))), **extra)
     dist.barrier()
     ctx.close()

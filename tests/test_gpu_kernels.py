@@ -23,14 +23,43 @@ def _same_plan(p, q):
     assert p.transfers == q.transfers
 
 
+def _plans_on_device(L, cases, ep=False):
+    """Run llep_plan_device on every (C [P, N] int32, alpha, m, lam) case: one device buffer holds all
+    load matrices and all output blobs, the launches are issued back to back on one stream (ctypes, no
+    per-case synchronisation), and the blobs come back in one copy.  -> list of blob bytes."""
+    import ctypes
+    dev = torch.device("cuda:0")
+    offs_in, offs_out, pos_in, pos_out = [], [], 0, 0
+    for (C, _a, _m, _l) in cases:
+        offs_in.append(pos_in)
+        pos_in += C.size * 4
+        offs_out.append(pos_out)
+        pos_out += (L.plan_bytes(C.shape[1], C.shape[0]) + 15) // 16 * 16
+    buf_in = np.zeros(max(pos_in, 4), dtype=np.uint8)
+    for (C, *_), o in zip(cases, offs_in):
+        buf_in[o:o + C.size * 4] = np.ascontiguousarray(C, dtype=np.int32).view(np.uint8).reshape(-1)
+    d_in = torch.from_numpy(buf_in).to(dev)
+    d_out = torch.zeros(max(pos_out, 16), dtype=torch.uint8, device=dev)
+    s = L._stream_ptr()
+    base_in, base_out = d_in.data_ptr(), d_out.data_ptr()
+    f = L._lib.llep_plan_device
+    for (C, a, m, lam), oi, oo in zip(cases, offs_in, offs_out):
+        prm = L.params(a, m, lam)
+        rc = f(base_in + oi, C.shape[1], C.shape[0], ctypes.byref(prm), int(ep), base_out + oo, s)
+        assert rc == 0, L._lib.llep_last_error()
+    out = d_out.cpu().numpy()
+    return [out[o:o + L.plan_bytes(C.shape[1], C.shape[0])].tobytes() for (C, *_), o in zip(cases, offs_out)]
+
+
 def test_device_planner_bit_exact(L):
-    """Device plan blob == host plan blob byte for byte, and == the oracle (O1) field by field."""
+    """10^4 random load matrices: device plan blob == host plan blob byte for byte, and == the oracle
+    (O1) field by field (chunks in order, g_a, cap, S, fallback, force_count, 𝒲), for LLEP and EP."""
     from oracle import planner as O1
     rng = random.Random(77)
-    dev = torch.device("cuda:0")
-    for i in range(600):
-        P = rng.choice([1, 2, 3, 4, 8, 16, 32])
-        M = rng.choice([1, 2, 4, 8, 16])
+    cases = []
+    while len(cases) < 10000:
+        P = rng.choice([1, 2, 3, 4, 8, 8, 16, 32])
+        M = rng.choice([1, 2, 4, 8, 16] + ([32, 64] if rng.random() < 0.05 else []))
         N = P * M
         if N > 1024:
             continue
@@ -42,14 +71,44 @@ def test_device_planner_bit_exact(L):
             C[p] = [rng.randint(0, 30) for _ in range(N)]
             if rng.random() < 0.7:
                 C[p, rng.randrange(N)] += rng.randint(100, 20000)
-        l = C.sum(0).astype(np.int64)
-        for ep in (False, True):
-            blob = L.plan_device(torch.from_numpy(C).to(dev), P, alpha, m, lam, ep=ep)
-            dp = L.parse_plan(blob.cpu().numpy().tobytes())
+        cases.append((C, alpha, m, lam))
+    for ep in (False, True):
+        blobs = _plans_on_device(L, cases, ep=ep)
+        for i, ((C, alpha, m, lam), blob) in enumerate(zip(cases, blobs)):
+            l = C.sum(0).astype(np.int64)
+            P = C.shape[0]
+            dp = L.parse_plan(blob)
             hp = L.plan_host(l, P, alpha, m, lam, ep=ep)
-            assert dp.raw == hp.raw, (i, P, N, alpha, m, lam, ep)
+            assert dp.raw == hp.raw, (i, P, C.shape[1], alpha, m, lam, ep)
             ref = O1.ep_plan(l, P, alpha, fallback=False) if ep else O1.plan(l.tolist(), P, alpha, m, lam)
             _same_plan(dp, ref)
+
+
+def test_device_planner_bruteforce_box(L):
+    """The brute-force box of SURVEY §8(c): every l in {0..7}^N for N <= 4 and P | N, α ∈ {1, 1.5, 2},
+    m ∈ {0, 1, 2, 3, 8}, λ ∈ {1, 1.3, ∞} (≈ 6·10^5 plans): the device planner equals O1 on every field."""
+    import itertools
+    from oracle import planner as O1
+    cases = []
+    for N in (1, 2, 3, 4):
+        for P in [p for p in (1, 2, 3, 4) if N % p == 0]:
+            for l in itertools.product(range(8), repeat=N):
+                C = np.zeros((P, N), dtype=np.int32)
+                C[0] = l
+                if P > 1:   # split the loads over the ranks (only column sums matter to the plan)
+                    C[P - 1] = np.array(l) // 2
+                    C[0] -= C[P - 1]
+                for alpha in (1.0, 1.5, 2.0):
+                    for m in (0, 1, 2, 3, 8):
+                        for lam in (1.0, 1.3, float("inf")):
+                            cases.append((C, alpha, m, lam))
+    assert len(cases) > 500000
+    for i0 in range(0, len(cases), 100000):
+        part = cases[i0:i0 + 100000]
+        blobs = _plans_on_device(L, part)
+        for (C, alpha, m, lam), blob in zip(part, blobs):
+            ref = O1.plan(C.sum(0).tolist(), C.shape[0], alpha, m, lam)
+            _same_plan(L.parse_plan(blob), ref)
 
 
 def _ref_gemm(mode, a, w, groups, nout, gate):

@@ -100,6 +100,9 @@ def test_multiprocess_p2_p4_one_gpu(L, tmp_path):
         dp = L.parse_plan(plans[0])
         assert [list(A) for A in dp.chunks] == [list(A) for A in ref_plan.chunks]
         assert len(ref_plan.transfers) > 0  # the spill path is exercised
+        LC.check_index_work(res, "llep", ref_plan, ids_all, sh.n_experts)
+        LC.check_index_work(res, "ep", O1.ep_plan(C.sum(0).tolist(), P, 1.0, fallback=False), ids_all,
+                            sh.n_experts)
         w = LC.OracleWeights(sh.d_model, sh.d_ff, 21)
         for p in range(P):
             ref = LC.oracle_rank_output(sh, p, ids_all[p], W.gate_weights(sh.tokens_per_rank, sh.top_k, p, 21), 21,
@@ -138,6 +141,7 @@ def test_multiprocess_force_assign_and_params(L, tmp_path, P, pct, nhot, params)
     assert dp.force_count == ref_plan.force_count
     if (P, pct) != (2, 95):
         assert ref_plan.force_count > 0
+    LC.check_index_work(res, "llep", ref_plan, ids_all, sh.n_experts)
     w = LC.OracleWeights(sh.d_model, sh.d_ff, 21)
     for p in range(P):
         ref = LC.oracle_rank_output(sh, p, ids_all[p], W.gate_weights(sh.tokens_per_rank, sh.top_k, p, 21), 21,
@@ -190,35 +194,69 @@ def test_g120_p1_sampled_parity(L):
 def test_large_layer_processes_one_gpu(L, tmp_path, cfg, P, pct, nhot, n_tr):
     """BASELINE shapes at full size with P ranks (processes sharing cuda:0, CUDA-IPC arenas),
     λ=1.3 α=1 m=1024.  Plan == oracle on every rank (expected weight-transfer count; EP fallback when
-    balanced), sampled outputs vs O3, LLEP == EP bitwise on every full output."""
+    balanced); the index work (load matrix, local ranks, group tables, every slot's (device, row)) of
+    the LLEP and EP calls bit-exact vs O2 on every rank; outputs vs O3 on a sample holding the tokens at
+    the first and last global index of every plan chunk (every chunk / group boundary of every device)
+    plus each rank's first 16 tokens; LLEP == EP bitwise on every full output."""
     from oracle import planner as O1
     from oracle import schedule as O2
-    S = 48
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29600 + pct + 7 * P + len(cfg)))
-    cmd = [sys.executable, os.path.join(HERE, "mp_layer_worker.py"), str(P), cfg, str(pct), str(nhot),
-           str(tmp_path), str(S)]
-    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1500)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    res = [np.load(os.path.join(tmp_path, f"rank{p}.npz")) for p in range(P)]
     sh0 = W.CONFIGS[cfg]
     sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, P)
     hot = None if pct == 0 else pct
     ids_all = [W.routing_ids(sh, p, hot, nhot, 21) for p in range(P)]
     C = O2.load_matrix(ids_all, sh.n_experts)
     ref_plan = O1.plan(C.sum(0).tolist(), P)
+    rows = LC.boundary_tokens(ref_plan, ids_all, sh.n_experts)
+    rows_file = os.path.join(tmp_path, "rows.npz")
+    np.savez(rows_file, **{f"r{p}": rows[p] for p in range(P)})
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29600 + pct + 7 * P + len(cfg)),
+               LLEP_TEST_ROWS=rows_file)
+    cmd = [sys.executable, os.path.join(HERE, "mp_layer_worker.py"), str(P), cfg, str(pct), str(nhot),
+           str(tmp_path)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = [np.load(os.path.join(tmp_path, f"rank{p}.npz")) for p in range(P)]
     plans = [bytes(r_["plan"].tobytes()) for r_ in res]
     assert all(p == plans[0] for p in plans)
     dp = L.parse_plan(plans[0])
     assert [list(A) for A in dp.chunks] == [list(A) for A in ref_plan.chunks]
     assert len(ref_plan.transfers) == n_tr and dp.fallback == (pct == 0)
+    LC.check_index_work(res, "llep", ref_plan, ids_all, sh.n_experts)
+    LC.check_index_work(res, "ep", O1.ep_plan(C.sum(0).tolist(), P, 1.0, fallback=False), ids_all, sh.n_experts)
     w = LC.OracleWeights(sh.d_model, sh.d_ff, 21)
-    rows = np.arange(S)
+    n_chunks = sum(len(A) for A in ref_plan.chunks)
+    assert sum(len(v) for v in rows.values()) >= min(n_chunks, 16 * P)
     for p in range(P):
         ref = LC.oracle_rank_output(sh, p, ids_all[p], W.gate_weights(sh.tokens_per_rank, sh.top_k, p, 21), 21,
-                                    rows=rows, weights=w)
+                                    rows=rows[p], weights=w)
         mr, l2 = LC.errors(res[p]["llep"].astype(np.float64), ref)
         assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (p, mr, l2)
         assert bool(res[p]["same"])
+
+
+def test_g120_p1_full_output_parity(L):
+    """BASELINE config G120 at the N=1 bench launch configuration (P=1, 32K tokens, 95 %/1): the WHOLE
+    [32768, 2880] output vs the float64 oracle O3 (6.5 TFLOP of float64 on the host; rows of each
+    expert processed in chunks), plus the index work (a1, a3, a5) bit-exact vs O2."""
+    from oracle import planner as O1
+    from oracle import schedule as O2
+    sh0 = W.CONFIGS["g120"]
+    sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, 1)
+    seed = 31
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, 95, 1, seed, "cuda")
+    ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, 1, 0, 0, sh.tokens_per_rank)
+    out = ctx(x, ids, gates, w13, w2)
+    torch.cuda.synchronize()
+    import mp_layer_worker as MW
+    res = [MW.dump_index_work(L, ctx, sh, 1, "llep")]
+    plan = O1.plan(O2.local_counts(ids_np, sh.n_experts).tolist(), 1)
+    LC.check_index_work(res, "llep", plan, [ids_np], sh.n_experts)
+    y = _to_np(out)
+    ctx.close()
+    del out, x, w13, w2
+    ref = LC.oracle_rank_output(sh, 0, ids_np, g_np, seed)
+    mr, l2 = LC.errors(y, ref)
+    assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (mr, l2)
 
 
 def test_memory_cap_nomem(L):
@@ -326,3 +364,54 @@ def test_peak_memory_bounded_by_plan(tmp_path):
     assert ll["max_rows"] == W.CONFIGS["g120"].tokens_per_rank * W.CONFIGS["g120"].top_k
     assert ll["peak_gb_per_gpu"] <= ll["model_gb_critical"] + 0.6, ll
     assert ll["model_gb_critical"] < line["ep"]["model_gb_critical"] / 3
+
+
+def test_forward_rejects_ids_other_than_prepared(L):
+    """§8(b) boundary: llep_moe_forward runs the plan, load matrix and local ranks of the LAST
+    llep_prepare.  A different topk_ids buffer with the same B -> LLEP_ERR_PLAN at once; the prepared
+    buffer modified in place -> the changed slots are dropped (every other token's output is still
+    exact) and llep_context_check reports LLEP_ERR_PLAN; the next prepare/forward is clean."""
+    sh = W.LayerShape(8, 2, 256, 512, 1024, 1)
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, 95, 1, 5, "cuda")
+    ctx = L.Context(8, 2, 256, 512, 1, 0, 0, 1024)
+    plan, _ = ctx.prepare(ids)
+    other = ids.clone()
+    other[:, 0] = (other[:, 0] + 1) % 8
+    with pytest.raises(L.LLEPError) as ei:
+        ctx.forward(x, other, gates, w13, w2, plan)
+    assert ei.value.code == 2
+    ctx.check()                                   # nothing ran: no sticky error
+    # in-place change of the prepared buffer after prepare: tokens 0..9 slot 1 -> another expert
+    ids_new = ids_np.copy()
+    ids_new[:10, 1] = (ids_new[:10, 1] + 3) % 8
+    ids.copy_(torch.from_numpy(ids_new).cuda())
+    out = ctx.forward(x, ids, gates, w13, w2, plan)
+    with pytest.raises(L.LLEPError) as ei:
+        ctx.check()
+    assert ei.value.code == 2
+    ctx.check()                                   # reported once, then cleared
+    y = _to_np(out)
+    g_drop = g_np.copy()
+    g_drop[:10, 1] = 0.0                          # the changed slots contribute nothing
+    ref = LC.oracle_rank_output(sh, 0, ids_np, g_drop, 5)
+    mr, l2 = LC.errors(y, ref)
+    assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (mr, l2)
+    # a fresh prepare on the new ids gives the exact output of the new routing
+    out2 = ctx(x, ids, gates, w13, w2)
+    ctx.check()
+    ref2 = LC.oracle_rank_output(sh, 0, ids_new, g_np, 5)
+    mr, l2 = LC.errors(_to_np(out2), ref2)
+    assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (mr, l2)
+    ctx.close()
+
+
+def test_asymmetric_arenas_rejected(tmp_path):
+    """ADVICE r1 (symmetric arena): two ranks whose contexts were created with different max_tokens
+    (raw C ABI, bypassing the binding's max-over-ranks) -> llep_context_open_peers fails with
+    LLEP_ERR_INVALID on both ranks instead of mapping arenas whose regions sit at different offsets."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29571")
+    cmd = [sys.executable, os.path.join(HERE, "mp_asym_worker.py"), str(tmp_path)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    codes = [int(np.load(os.path.join(tmp_path, f"asym{p}.npy"))) for p in range(2)]
+    assert codes == [1, 1], codes

@@ -46,6 +46,44 @@ def test_materialize_example(golden_dir):
         assert [list(s) for s in sch[(p, e)]] == sl
 
 
+def test_global_index_rank_major_worked_example(golden_dir):
+    """R11 / S:253 (rank-major global order): expert e0 has counts [6, 4] on ranks 0 and 1, so rank 0's
+    six slots of e0 take global indices 0..5 and rank 1's four take 6..9 (a reversed rank order,
+    Σ_{q>p}, would give rank 0 indices 4..9).  Under S:253's plan e0 -> [(0,0,5),(1,5,10)], rank 0's
+    local [0,5) goes to device 0 rows 0..4, its local [5,6) to device 1 row 0, and rank 1's local
+    [0,4) to device 1 rows 1..4 (chunks of e0 on device 1 concatenated in plan order)."""
+    ex = _load(golden_dir, "schedule_examples.json")["materialize"][0]
+    C = np.array(ex["C"])
+    # K = 1: rank 0 holds six tokens routed to e0, rank 1 four (C's e1 column is empty)
+    ids0 = np.array([[0], [0], [0], [0], [0], [0]])
+    ids1 = np.array([[0], [0], [0], [0]])
+    assert O2.global_index(ids0, C, 0).tolist() == [0, 1, 2, 3, 4, 5]
+    assert O2.global_index(ids1, C, 1).tolist() == [6, 7, 8, 9]
+    plan = O1.Plan(2, 2, [[tuple(c) for c in A] for A in ex["chunks"]], [5, 5], 5, 10, False)
+    d0, r0 = O2.slot_destinations(plan, C, ids0, 0)
+    d1, r1 = O2.slot_destinations(plan, C, ids1, 1)
+    assert d0.tolist() == [0, 0, 0, 0, 0, 1] and r0.tolist() == [0, 1, 2, 3, 4, 0]
+    assert d1.tolist() == [1, 1, 1, 1] and r1.tolist() == [1, 2, 3, 4]
+    # with K = 2 and other experts interleaved the index counts only e's own earlier slots
+    C2 = np.array([[2, 3], [1, 2]])
+    ids_r1 = np.array([[1, 0], [1, 1]])     # flat slots: e1, e0, e1, e1
+    assert O2.global_index(ids_r1, C2, 1).tolist() == [3, 2, 4, 5]
+
+
+def test_relative_errors_hand_values():
+    """R21: max_rel = max|y-r| / max|r| and rel_L2 = ||y-r||_2 / ||r||_2 over the WHOLE output.
+    y=[1,2], r=[1,1]: diff [0,1] -> max_rel 1, rel_L2 1/sqrt(2).  y=[2,0], r=[4,2]: max_rel 2/4 (a
+    y-normaliser would give 1), rel_L2 sqrt(8/20).  2-D: the max is over all elements, not per row
+    (a per-row normaliser would give 1 for the first row)."""
+    mr, l2 = O3.relative_errors(np.array([1.0, 2.0]), np.array([1.0, 1.0]))
+    assert mr == 1.0 and l2 == pytest.approx(1 / math.sqrt(2), rel=1e-15)
+    mr, l2 = O3.relative_errors(np.array([2.0, 0.0]), np.array([4.0, 2.0]))
+    assert mr == 0.5 and l2 == pytest.approx(math.sqrt(0.4), rel=1e-15)
+    mr, l2 = O3.relative_errors(np.array([[1.0, 0.0], [10.0, 10.0]]), np.array([[1.0, 1.0], [10.0, 10.0]]))
+    assert mr == 0.1 and l2 == pytest.approx(1 / math.sqrt(202), rel=1e-15)
+    assert O3.relative_errors(np.array([3.0, -4.0]), np.array([3.0, -4.0])) == (0.0, 0.0)
+
+
 def test_out_of_range_ids():
     with pytest.raises(ValueError):
         O2.local_counts(np.array([[0, 5]]), 4)

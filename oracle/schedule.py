@@ -45,18 +45,13 @@ def stable_reindex(ids: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
 
 def local_rank_in_expert(ids: np.ndarray) -> np.ndarray:
     """r_j = #{j' < j : ids[j'] = ids[j]} for every flat slot j (position inside the
-    rank's own per-expert batch B_i of P:282)."""
+    rank's own per-expert batch B_i of P:282): in the stable sorted order, a slot's rank is its
+    sorted position minus the sorted position of the first slot of its expert."""
     flat = np.asarray(ids).reshape(-1)
     perm, sorted_ids = stable_reindex(flat)
+    first = np.searchsorted(sorted_ids, sorted_ids, side="left")   # start of each slot's expert run
     r = np.empty(flat.size, dtype=np.int64)
-    start = 0
-    n = flat.size
-    while start < n:
-        end = start
-        while end < n and sorted_ids[end] == sorted_ids[start]:
-            end += 1
-        r[perm[start:end]] = np.arange(end - start)
-        start = end
+    r[perm] = np.arange(flat.size) - first
     return r
 
 
@@ -80,26 +75,25 @@ def rows_on_device(plan: Plan, e: int, d: int) -> int:
 
 
 def slot_destinations(plan: Plan, C: np.ndarray, ids: np.ndarray, rank: int) -> Tuple[np.ndarray, np.ndarray]:
-    """For each flat slot j of rank p: destination device d_j and the slot's position
-    among expert e's rows on d_j (chunks of e on d concatenated in plan order)."""
+    """For each flat slot j of rank p: destination device d_j (the device of the unique chunk of
+    expert e_j with start <= gidx_j < end) and the slot's position among expert e_j's
+    rows on d_j (the chunks of e on d concatenated in plan order: the chunk's offset among them
+    plus gidx_j - start)."""
     flat = np.asarray(ids).reshape(-1)
     g = global_index(flat, C, rank)
-    dev = np.empty(flat.size, dtype=np.int64)
+    dev = np.full(flat.size, -1, dtype=np.int64)
     pos = np.empty(flat.size, dtype=np.int64)
-    for j in range(flat.size):
-        e = int(flat[j])
-        off_on = {}
-        found = False
-        for (d0, s, t) in plan.chunks[e]:
+    for e in np.unique(flat):
+        of_e = flat == e
+        off_on = {}                                   # rows of e's earlier chunks on each device
+        for (d0, s, t) in plan.chunks[int(e)]:
             base = off_on.get(d0, 0)
-            if s <= g[j] < t:
-                dev[j] = d0
-                pos[j] = base + (g[j] - s)
-                found = True
-                break
+            hit = of_e & (g >= s) & (g < t)
+            dev[hit] = d0
+            pos[hit] = base + (g[hit] - s)
             off_on[d0] = base + (t - s)
-        if not found:
-            raise ValueError("uncovered slot")
+    if flat.size and (dev < 0).any():
+        raise ValueError("uncovered slot")
     return dev, pos
 
 

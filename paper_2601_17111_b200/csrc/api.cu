@@ -192,6 +192,8 @@ struct llep_context {
   int32_t *dev_padded = nullptr, *dev_foreign = nullptr;
   Group *groups = nullptr;
   int32_t *sched = nullptr;
+  uint32_t *mblk_src = nullptr;           // [sched_cap] row f2: sources of each m-block
+  uint32_t *block_done = nullptr;         // dispatch_kernel's finished-block count
   int64_t sched_cap = 0;
   LayoutSummary *summary = nullptr;
   LayoutSummary *summary_host = nullptr;  // mapped pinned (written by mirror_kernel)
@@ -222,6 +224,7 @@ struct llep_context {
   void **d_ptrs = nullptr;  // device: flags[P], lm[P], x[P], g[P], o[P], grad[P]
   uint32_t epoch = 0;
   uint32_t wepoch = 0;      // row f2: weight-flag epoch, one per forward call (same on every rank)
+  uint32_t aepoch = 0;      // row f2: dispatch-arrival epoch, one per forward call
   // host copy of the last prepared plan
   std::vector<uint8_t> plan_host;
   const void *plan_dev_cached = nullptr;
@@ -272,7 +275,7 @@ static ArenaGeometry geometry(const llep_context *c);
 static void layout_offsets(llep_context *c, int64_t rows, int32_t foreign) {
   size_t off = kGeomBytes;
   c->off_flags = off;
-  off += 4 * (kWeightFlag0 + kMaxGroups);
+  off += 4 * kFlagWords;
   c->off_lm = off;
   off = align8(off + sizeof(int32_t) * (size_t)c->P * c->N);
   off = (off + 1023) & ~size_t(1023);
@@ -509,6 +512,9 @@ llep_status llep_context_create(const llep_shape *s, int32_t rank, int32_t devic
   // worst case: every slot of every rank lands on this device, plus one partial block per group
   c->sched_cap = ((int64_t)P * slots + kRowAlign - 1) / kRowAlign + kMaxGroups;
   if (!e) e = A(&c->sched, sizeof(int32_t) * c->sched_cap);
+  if (!e) e = A(&c->mblk_src, sizeof(uint32_t) * c->sched_cap);
+  if (!e) e = A(&c->block_done, sizeof(uint32_t));
+  if (!e) e = cudaMemset(c->block_done, 0, sizeof(uint32_t));
   if (!e) e = A(&c->summary, sizeof(LayoutSummary));
   if (!e) e = A(&c->d_ptrs, sizeof(void *) * 8 * P);
   if (!e) e = cudaMemset(c->err, 0, sizeof(int32_t) * 4);
@@ -540,7 +546,7 @@ void llep_context_destroy(llep_context *c) {
   close_peers(c);
   void *ptrs[] = {c->tile_cnt, c->tile_off, c->cnt, c->local_rank, c->prep_ids, c->slot_dst, c->err,
                   c->lm_local, c->rows_on, c->chunk_row, c->foreign_slot, c->dev_padded,
-                  c->dev_foreign, c->groups, c->sched, c->summary, c->d_ptrs, c->act, c->arena,
+                  c->dev_foreign, c->groups, c->sched, c->mblk_src, c->block_done, c->summary, c->d_ptrs, c->act, c->arena,
                   c->gu, c->da0, c->aw, c->dgu, c->stage13, c->stage2, c->wsbuf, c->dotp};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -702,6 +708,7 @@ static llep_status run_layout(llep_context *c, const void *plan, cudaStream_t s)
   la.sched = c->sched;
   la.sched_cap = c->sched_cap;
   la.row_align = c->row_align;
+  la.mblk_src = c->mblk_src;
   LLEP_CUDA(launch_layout(la, s));
   ++c->launches;
   return LLEP_OK;
@@ -924,9 +931,18 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   da.x2 = nullptr;
   da.peer_x2 = nullptr;
   da.peer_rsrc = reinterpret_cast<int32_t *const *>(c->d_ptrs + 6 * P);
+  // row f2: no barrier between the dispatch and GEMM1.  The dispatch publishes a per-source arrival
+  // flag on every device once all of its rows are stored; GEMM1's producers wait, per m-block, only
+  // for the sources of that block's rows (and, per foreign group, for its weight flag), so tiles start
+  // as their inputs land instead of after the slowest rank (LLEP_DISPATCH_BARRIER=1: old barrier)
+  const bool overlap = P > 1 && !getenv("LLEP_DISPATCH_BARRIER");
+  const uint32_t aepoch = ++c->aepoch;
+  da.peer_flags = overlap ? peer_flags(c) : nullptr;
+  da.epoch = aepoch;
+  da.block_done = c->block_done;
   LLEP_CUDA(launch_dispatch(da, s));
-  c->launches += B > 0;
-  if ((st = barrier(c, s)) != LLEP_OK) return st;   // dispatched rows landed (weights: flags)
+  c->launches += B > 0 || overlap;
+  if (!overlap && (st = barrier(c, s)) != LLEP_OK) return st;   // dispatched rows landed
   mark(c, 5, s);
   // a8: GEMM1 + SwiGLU   X [rows, D] -> A [rows, H]
   uint16_t *X = reinterpret_cast<uint16_t *>(c->arena + c->off_x);
@@ -951,6 +967,9 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   g1.wflags = P > 1 ? reinterpret_cast<const uint32_t *>(c->arena + c->off_flags) + kWeightFlag0 : nullptr;
   g1.wepoch = wepoch;
   g1.err = c->err;
+  g1.arrive = overlap ? reinterpret_cast<const uint32_t *>(c->arena + c->off_flags) + kArriveFlag0 : nullptr;
+  g1.aepoch = aepoch;
+  g1.mblk_src = c->mblk_src;
   g1.row_src = nullptr;
   g1.peer_slot = nullptr;
   g1.num_sms = c->num_sms;
@@ -1122,6 +1141,9 @@ static llep_status moe_backward(llep_context *c, const uint16_t *x, const int32_
   da.x2 = dout;
   da.peer_x2 = reinterpret_cast<uint16_t *const *>(c->d_ptrs + 4 * P);
   da.peer_rsrc = nullptr;
+  da.peer_flags = nullptr;   // the backward keeps its barrier (weights and rows joined before the GEMMs)
+  da.epoch = 0;
+  da.block_done = c->block_done;
   LLEP_CUDA(launch_dispatch(da, s));
   c->launches += B > 0;
   if (any_copy) LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));

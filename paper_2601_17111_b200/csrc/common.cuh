@@ -121,6 +121,8 @@ struct LayoutArgs {
   int32_t *sched;              // [sched_cap] this rank's m-block order (sched_pack)
   int64_t sched_cap;
   int32_t row_align;           // group row bases / GEMM M tile: 128 or 256
+  uint32_t *mblk_src;          // [sched_cap] per m-block (group order) of this rank: bit q set iff the
+                               // block holds rows dispatched by source rank q (row f2 arrival waits)
 };
 
 // kernel launchers (route.cu / plan.cu / gemm.cu)
@@ -148,7 +150,10 @@ cudaError_t launch_grad_reduce(float *dst, const float *base, int n_src, int64_t
                                cudaStream_t s);
 cudaError_t launch_signal(uint32_t *flag, uint32_t v, cudaStream_t s);
 cudaError_t launch_wait_flag(const uint32_t *flag, uint32_t v, int32_t *err, cudaStream_t s);
-constexpr int kWeightFlag0 = 32;   // arena flag words: [0, 32) barrier, [32, 32 + kMaxGroups) weight slots
+constexpr int kWeightFlag0 = 32;   // arena flag words: [0, 32) barrier, [32, 32 + kMaxGroups) weight slots,
+constexpr int kArriveFlag0 = kWeightFlag0 + kMaxGroups;   // then [32) dispatch arrivals (one per source)
+constexpr int kFlagWords = kArriveFlag0 + kMaxWorld;
+cudaError_t launch_arrive(uint32_t *const *peer_flags, int32_t rank, int32_t P, uint32_t epoch, cudaStream_t s);
 cudaError_t launch_combine_local(const uint16_t *slotbuf, int64_t B, int K, int D, const int32_t *slot_dst,
                                  uint16_t *out, cudaStream_t s);
 cudaError_t launch_mirror(const void *plan, size_t plan_bytes, const void *summary, size_t sum_bytes,
@@ -173,6 +178,12 @@ struct DispatchArgs {
   const uint16_t *x2;       // optional second row source (backward: the upstream gradient dOut)
   uint16_t *const *peer_x2; // [P] its receive rows
   int32_t *const *peer_rsrc;  // optional [P] per receive row: (flat slot << 5) | source rank
+  // row f2 (dispatch overlapped with the GEMMs): when peer_flags is set, the last block to finish
+  // publishes `epoch` into arrival flag [rank] of every device (release, system scope) once all of this
+  // rank's rows are stored; block_done counts finished blocks (rank-local, returns to 0)
+  uint32_t *const *peer_flags;
+  uint32_t epoch;
+  uint32_t *block_done;
 };
 cudaError_t launch_dispatch(const DispatchArgs &a, cudaStream_t s);
 
@@ -209,6 +220,9 @@ struct GemmArgs {
   uint32_t wepoch;           //         (nullptr: weights already resident)
   int32_t *err;              //         err[1] |= 16 if a weight wait times out (~20 s); waits are
                              //         skipped once err[1] is set (a peer failed: no hang)
+  const uint32_t *arrive;    // row f2: this rank's dispatch arrival flags [P] (nullptr: rows resident)
+  uint32_t aepoch;           //         source q's rows landed when arrive[q] >= aepoch
+  const uint32_t *mblk_src;  //         per m-block (group order): mask of the sources of its rows
   const int32_t *row_src;    // mode 1 push epilogue: (slot << 5) | rank of each receive row, and
   uint16_t *const *peer_slot;//   [P] slot buffers [B*K, nout]: the row's output goes to
                              //   peer_slot[rank] + slot*nout (nullptr: write `out` rows)

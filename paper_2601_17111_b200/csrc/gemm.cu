@@ -61,6 +61,9 @@ struct GemmParams {
   const uint32_t *wflags;
   uint32_t wepoch;
   int32_t *err;
+  const uint32_t *arrive;
+  uint32_t aepoch;
+  const uint32_t *mblk_src;
   const int32_t *row_src;
   uint16_t *const *peer_slot;
   __nv_bfloat16 *out2;   // mode 3: raw [g | u] pre-activations, rows of 2 * nout (training forward)
@@ -91,6 +94,36 @@ __device__ __forceinline__ void wait_weights(const GemmParams &p, int wslot) {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Row f2: the dispatch is overlapped with the GEMMs.  Before the first TMA load of an m-block's
+// activation rows, wait until every source rank that dispatched rows into that block has published
+// its arrival flag (release after all its rows were stored, route.cu dispatch_kernel), then order the
+// async-proxy (TMA) reads after the acquire.  Bounded like wait_weights.
+__device__ __forceinline__ void wait_sources(const GemmParams &p, int mblk, uint32_t &seen) {
+  if (!p.arrive) return;
+  uint32_t need = p.mblk_src[mblk] & ~seen;
+  if (!need) return;
+  const long long t0 = clock64();
+  long long spins = 0;
+  while (need) {
+    const int q = __ffs(need) - 1;
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p.arrive + q) : "memory");
+    if ((int32_t)(v - p.aepoch) >= 0) {
+      need &= need - 1;
+      seen |= 1u << q;
+      continue;
+    }
+    if (((++spins) & 255) == 0) {
+      if (p.err && *reinterpret_cast<volatile int32_t *>(p.err + 1) != 0) break;
+      if (clock64() - t0 > 40000000000LL) {
+        if (p.err) atomicOr(p.err + 1, 32);
+        break;
+      }
+    }
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
@@ -114,6 +147,7 @@ __device__ __forceinline__ uint32_t instr_desc() {
 
 struct TileInfo {
   int row0, row_end, nb, wslot, small;
+  int mblk;   // m-block index in group order (Group.mblk_start + m)
   int half;   // pair kernel: <= 128 rows left in this block -> M=128 pair MMA (64 rows per CTA)
   int swap;   // pair kernel: <= 64 rows -> swapped tile, D[weight rows x tokens] (M=256, N=64)
 };
@@ -141,6 +175,7 @@ __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int *
     m = mb - s_mblk[lo];
   }
   const Group g = groups[lo];
+  ti.mblk = g.mblk_start + m;
   ti.row0 = g.row_base + m * TM;
   ti.row_end = g.row_base + g.n_rows;
   ti.wslot = g.wslot;
@@ -206,11 +241,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
       // ---------------------------------------------------------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
+      uint32_t seen = 0;   // sources whose arrival this thread already acquired
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         const TileInfo ti = decode_tile(t, p.n_ntiles, s_mblk, n_groups, p.groups, p.sched);
         const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
         const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
         wait_weights(p, ti.wslot);
+        wait_sources(p, ti.mblk, seen);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const uint32_t fb = smem_u32(full + stage);
@@ -343,6 +380,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
       if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
     }
   }
+  // fused combine push (mode 1): order this thread's peer stores before the kernel's completion and
+  // the device barrier that follows (release at system scope there; per-thread fence here)
+  if (MODE == 1 && p.peer_slot) asm volatile("fence.acq_rel.sys;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -467,6 +507,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       const uint64_t pol_act = l2_policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
+      uint32_t seen = 0;   // sources whose arrival this thread already acquired
       for (int t = pair; t < total_tiles; t += n_pairs) {
         TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
         ti.swap = p.swap && ti.row_end - ti.row0 <= 64;
@@ -474,6 +515,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
         const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
         const int brow = MODE != 1 ? wbase + (int)crank * p.wup_off : wbase + (int)crank * (BN / 2);
         wait_weights(p, ti.wslot);
+        wait_sources(p, ti.mblk, seen);
         // swapped tile: this CTA's 128 weight rows as the A operand (mode 0/2/3: 64 gate + the
         // matching 64 up rows of features nb*BNO + crank*64 ...; mode 1: rows nb*BN + crank*BN/2
         // ...) and its 32 of the group's <= 64 token rows as the B operand
@@ -899,6 +941,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(tempty + acc), 0));
     }
   }
+  // fused combine push (mode 1): order this thread's peer stores before the kernel's completion and
+  // the device barrier that follows (release at system scope there; per-thread fence here)
+  if (MODE == 1 && p.peer_slot) asm volatile("fence.acq_rel.sys;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();
@@ -2026,6 +2071,9 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   prm.wflags = g.wflags;
   prm.wepoch = g.wepoch;
   prm.err = g.err;
+  prm.arrive = g.arrive;
+  prm.aepoch = g.aepoch;
+  prm.mblk_src = g.mblk_src;
   prm.row_src = g.row_src;
   prm.peer_slot = g.peer_slot;
   prm.n_groups_dev = g.n_groups_dev;

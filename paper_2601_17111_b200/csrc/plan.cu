@@ -383,6 +383,43 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(LayoutArgs a) {
       a.sched[pos] = sched_pack(lo, m);
     }
   }
+  // row f2: sources of every m-block of this rank (group order).  Group rows are e's chunks on this
+  // device in plan order; a chunk (d, s, t) holds global indices [s, t) of e, and source q owns
+  // [Σ_{p<q} C[p][e], Σ_{p<=q} C[p][e]) of them (rank-major order, R11), so the block's rows map to
+  // global ranges whose overlap with each source's range decides the mask.
+  if (a.mblk_src && sm_mblocks <= a.sched_cap && sm_groups <= kMaxGroups) {
+    for (int mb = tid; mb < sm_mblocks; mb += kLayoutThreads) {
+      int lo = 0, hi = sm_groups - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.groups[mid].mblk_start <= mb) lo = mid;
+        else hi = mid - 1;
+      }
+      const Group g = a.groups[lo];
+      const int r0 = (mb - g.mblk_start) * a.row_align;
+      const int r1 = min(r0 + a.row_align, g.n_rows);
+      const int e = g.expert;
+      uint32_t mask = 0;
+      int off = 0;
+      for (int c = 0; c < n_chunks[e] && c < MC; ++c) {
+        const llep_chunk ch = chunks[(size_t)e * MC + c];
+        if (ch.device != a.rank) continue;
+        const int len = ch.end - ch.start;
+        const int x0 = max(r0, off), x1 = min(r1, off + len);
+        if (x0 < x1) {
+          const long long g0 = ch.start + (x0 - off), g1 = ch.start + (x1 - off);   // global [g0, g1)
+          long long cum = 0;
+          for (int q = 0; q < P; ++q) {
+            const long long nq = a.load_matrix[(size_t)q * N + e];
+            if (nq > 0 && cum < g1 && cum + nq > g0) mask |= 1u << q;
+            cum += nq;
+          }
+        }
+        off += len;
+      }
+      a.mblk_src[mb] = mask;
+    }
+  }
   // destination row of each chunk's first token: group base + rows of e's earlier chunks on d
   for (int e = tid; e < N; e += kLayoutThreads) {
     const int nc = n_chunks[e];

@@ -168,10 +168,36 @@ __global__ void barrier_kernel(uint32_t *const *__restrict__ peer_flags, int ran
 // x[t] once (16-byte loads) and stores it to each of the K destinations (peer-mapped rows).
 constexpr int kDispatchWarps = 8;
 
+__device__ __forceinline__ void dispatch_token(const DispatchArgs &a, int64_t t, int lane);
+
+// Ordering of the peer stores (multi-GPU): every thread orders its own row / gate / source stores
+// before the block's completion count with fence.acq_rel.sys; the last block acquires all counts
+// (atom.acq_rel) and releases `epoch` into every destination's arrival flag [rank] at system scope, so
+// a destination that acquires the flag sees every row this rank dispatched to it (cumulativity).
 __global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_kernel(DispatchArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * kDispatchWarps + (threadIdx.x >> 5);
-  if (t >= a.B) return;
+  if (t < a.B) dispatch_token(a, t, lane);
+  if (!a.peer_flags) return;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.block_done) : "memory");
+    if (prev == gridDim.x - 1) {
+      *a.block_done = 0;   // next call's count (stream-ordered after this kernel)
+      for (int q = 0; q < a.P; ++q) st_release_sys(a.peer_flags[q] + kArriveFlag0 + a.rank, a.epoch);
+    }
+  }
+}
+
+// P=1 or a rank without tokens: publish the arrival flags alone
+__global__ void arrive_kernel(uint32_t *const *__restrict__ peer_flags, int rank, int P, uint32_t epoch) {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (int q = threadIdx.x; q < P; q += blockDim.x) st_release_sys(peer_flags[q] + kArriveFlag0 + rank, epoch);
+}
+
+__device__ __forceinline__ void dispatch_token(const DispatchArgs &a, int64_t t, int lane) {
   const int K = a.K, N = a.N, P = a.P, MC = P + 1;
   const uint8_t *plan = reinterpret_cast<const uint8_t *>(a.plan);
   const PlanLayout L = plan_layout(N, P);
@@ -610,8 +636,13 @@ cudaError_t launch_barrier(uint32_t *const *peer_flags, int32_t rank, int32_t P,
   return cudaGetLastError();
 }
 
+cudaError_t launch_arrive(uint32_t *const *peer_flags, int32_t rank, int32_t P, uint32_t epoch, cudaStream_t s) {
+  arrive_kernel<<<1, 32, 0, s>>>(peer_flags, rank, P, epoch);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dispatch(const DispatchArgs &a, cudaStream_t s) {
-  if (a.B == 0) return cudaSuccess;
+  if (a.B == 0) return a.peer_flags ? launch_arrive(a.peer_flags, a.rank, a.P, a.epoch, s) : cudaSuccess;
   const int64_t blocks = (a.B + kDispatchWarps - 1) / kDispatchWarps;
   dispatch_kernel<<<(unsigned)blocks, kDispatchWarps * 32, 0, s>>>(a);
   return cudaGetLastError();

@@ -35,6 +35,21 @@ class OracleWeights:
         self.D, self.H, self.seed = D, H, seed
         self.cache = {}
 
+    def prefetch(self, experts, threads: int = 0):
+        """Generate the weights of many experts in parallel (numpy releases the GIL in its ufuncs)."""
+        from concurrent.futures import ThreadPoolExecutor
+        todo = sorted({int(e) for e in experts} - set(self.cache))
+        if not todo:
+            return
+        n = threads or min(32, os.cpu_count() or 1)
+        with ThreadPoolExecutor(max_workers=n) as ex:
+            for e, w in zip(todo, ex.map(self._make, todo)):
+                self.cache[e] = w
+
+    def _make(self, e: int):
+        wg, wu, wd = W.expert_weights_bits(e, self.D, self.H, self.seed)
+        return (W.bf16_bits_to_f64(wg), W.bf16_bits_to_f64(wu), W.bf16_bits_to_f64(wd))
+
     def __call__(self, e: int):
         if e not in self.cache:
             wg, wu, wd = W.expert_weights_bits(e, self.D, self.H, self.seed)
@@ -52,6 +67,8 @@ def oracle_rank_output(shape: W.LayerShape, rank: int, ids: np.ndarray, gates: n
     xb = W.token_rows_bits(rows, D, rank, seed) if len(rows) < ids.shape[0] else W.tokens_bits(ids.shape[0], D, rank, seed)
     x = W.bf16_bits_to_f64(xb)
     weights = weights or OracleWeights(D, H, seed)
+    if hasattr(weights, "prefetch"):
+        weights.prefetch(np.unique(ids[rows]))
     return O3.moe_forward(x, ids[rows], gates[rows].astype(np.float64), weights)
 
 

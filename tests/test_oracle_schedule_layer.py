@@ -273,3 +273,69 @@ def test_generator_numpy_torch_identical():
     f = np.array([1.0, 1.00390625, 1.01171875, -3.0e-39, 65504.0, 1e30], dtype=np.float32)
     assert np.array_equal(W.bf16_bits_from_f32(f),
                           torch.from_numpy(f).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16))
+
+
+def test_distinct_routing_generator():
+    """SPEC generate_routing: K distinct ids per token by weighted sampling without replacement.
+    With K=1 it is plain categorical sampling, so the hot expert's share approaches x (95 %); with K=4 a
+    token can hold the hot expert once, so its share is capped at 1/K; deterministic per seed."""
+    sh1 = W.LayerShape(128, 1, 64, 64, 20000, 1)
+    ids = W.routing_ids(sh1, 0, 95, 1, distinct=True)
+    assert abs((ids == 0).mean() - 0.95) < 0.01
+    sh = W.LayerShape(128, 4, 64, 64, 4096, 1)
+    ids = W.routing_ids(sh, 0, 95, 1, distinct=True)
+    assert ids.shape == (4096, 4) and ids.dtype == np.int32
+    assert all(len(set(r.tolist())) == 4 for r in ids)
+    assert (ids == 0).any(axis=1).mean() > 0.99 and (ids == 0).mean() <= 0.25
+    assert np.array_equal(ids, W.routing_ids(sh, 0, 95, 1, distinct=True))
+    bal = W.routing_ids(W.LayerShape(8, 2, 64, 64, 40000, 1), 0, None, 0, distinct=True)
+    c = np.bincount(bal.ravel(), minlength=8)
+    assert np.all(np.abs(c - 10000) < 5 * np.sqrt(10000))
+
+
+def _loop_local_rank(flat):
+    seen, r = {}, []
+    for e in flat.tolist():
+        r.append(seen.get(e, 0))
+        seen[e] = seen.get(e, 0) + 1
+    return r
+
+
+def _loop_destinations(plan, C, flat, rank):
+    """Slot-by-slot transcription of S:247-255 (independent of O2's vectorised form)."""
+    before = [int(C[:rank, e].sum()) for e in range(C.shape[1])]
+    seen, dev, pos = {}, [], []
+    for e in flat.tolist():
+        g = before[e] + seen.get(e, 0)
+        seen[e] = seen.get(e, 0) + 1
+        off = {}
+        for (d0, s, t) in plan.chunks[e]:
+            if s <= g < t:
+                dev.append(d0)
+                pos.append(off.get(d0, 0) + g - s)
+                break
+            off[d0] = off.get(d0, 0) + t - s
+    return dev, pos
+
+
+def test_schedule_vectorised_equals_slot_loop():
+    """O2's local ranks and destinations equal a plain per-slot loop (counting seen slots, walking the
+    chunks) on random plans with spills, forces, zero-load experts and duplicate ids."""
+    rng = np.random.default_rng(17)
+    for trial in range(80):
+        P = int(rng.choice([1, 2, 3, 4, 8]))
+        N = P * int(rng.integers(1, 5))
+        K = int(rng.integers(1, 5))
+        ids = []
+        for p in range(P):
+            x = rng.integers(0, N, size=(int(rng.integers(0, 60)), K))
+            x[rng.random(x.shape) < 0.5] = int(rng.integers(0, N))
+            ids.append(x.astype(np.int32))
+        C = O2.load_matrix(ids, N)
+        plan = O1.plan(C.sum(0).tolist(), P, float(rng.choice([1.0, 1.5])), int(rng.choice([0, 2, 9])), 1.0)
+        for p in range(P):
+            flat = ids[p].reshape(-1)
+            assert O2.local_rank_in_expert(flat).tolist() == _loop_local_rank(flat)
+            dev, pos = O2.slot_destinations(plan, C, ids[p], p)
+            d2, p2 = _loop_destinations(plan, C, flat, p)
+            assert dev.tolist() == d2 and pos.tolist() == p2

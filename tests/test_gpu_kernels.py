@@ -137,6 +137,9 @@ def _ref_gemm(mode, a, w, groups, nout, gate):
     (0, 128, 144),    # masked tail tiles at other widths
     (1, 256, 288),
     (0, 136, 264),
+    (0, 7168, 2048),  # DeepSeek-V3 / Kimi-K2 GEMM1 (row f3: D=7168 -> 56 K-stages of 128)
+    (1, 2048, 7168),  # DeepSeek-V3 / Kimi-K2 GEMM2 (nout 7168 = 28 tiles of 256)
+    (0, 2048, 2048),  # F-head GEMM1
 ])
 def test_grouped_gemm(L, mode, kdim, nout, pair):
     g = torch.Generator(device="cuda").manual_seed(kdim * 7 + nout)

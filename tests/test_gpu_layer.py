@@ -450,3 +450,70 @@ def test_dispatch_overlap_matches_barrier(L, tmp_path):
         outs[mode] = [np.load(os.path.join(d, f"rank{p}.npz"))["llep"] for p in range(4)]
     for a, b in zip(outs["overlap"], outs["barrier"]):
         assert np.array_equal(a, b)
+
+
+def _few_expert_rows(ids_np, n_experts_max, head=40, tail=24):
+    """Tokens whose K experts all lie in 0..n_experts_max-1 (the hot expert and a few cold ones), the
+    first `head` and last `tail` of them: few experts' weights for the float64 oracle."""
+    ok = np.nonzero((ids_np < n_experts_max).all(1))[0]
+    return np.unique(np.concatenate([ok[:head], ok[-tail:]]))
+
+
+@pytest.mark.parametrize("cfg", ["dsv3", "kimi", "fhead"])
+def test_f3_shapes_p1_sampled_parity(L, cfg):
+    """Row f3: the paper's other layer shapes at P=1, 95 %/1 -- DeepSeek-V3 (N=256, K=8, D=7168, H=2048,
+    16K), Kimi-K2 (N=384, same dims) (F-models) and the F-head layer (N=128, K=4, D=H=2048,
+    32K): sampled outputs vs O3 and the index work (a1, a3, a5) bit-exact vs O2."""
+    from oracle import planner as O1
+    from oracle import schedule as O2
+    import mp_layer_worker as MW
+    sh0 = W.CONFIGS[cfg]
+    sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, 1)
+    seed = 43
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, 95, 1, seed, "cuda")
+    ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, 1, 0, 0, sh.tokens_per_rank)
+    out = ctx(x, ids, gates, w13, w2)
+    ctx.check()
+    res = [MW.dump_index_work(L, ctx, sh, 1, "llep")]
+    LC.check_index_work(res, "llep", O1.plan(O2.local_counts(ids_np, sh.n_experts).tolist(), 1), [ids_np],
+                        sh.n_experts)
+    rows = _few_expert_rows(ids_np, 12)
+    y = _to_np(out[torch.from_numpy(rows).cuda()])
+    ctx.close()
+    del out, w13, w2
+    ref = LC.oracle_rank_output(sh, 0, ids_np, g_np, seed, rows=rows)
+    mr, l2 = LC.errors(y, ref)
+    assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (cfg, mr, l2)
+
+
+def test_f3_dsv3_p4_processes(L, tmp_path):
+    """Row f3 at EP 4: the DeepSeek-V3-shaped layer (N=256, K=8, D=7168, H=2048, 16K tokens/rank), 95 %/1,
+    four processes sharing cuda:0.  Plan == O1 on every rank, index work bit-exact vs O2 for LLEP and
+    EP, sampled outputs vs O3 (tokens whose experts all lie in 0..11), LLEP == EP bitwise."""
+    from oracle import planner as O1
+    from oracle import schedule as O2
+    P, cfg = 4, "dsv3"
+    sh0 = W.CONFIGS[cfg]
+    sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, P)
+    ids_all = [W.routing_ids(sh, p, 95, 1, 21) for p in range(P)]
+    C = O2.load_matrix(ids_all, sh.n_experts)
+    ref_plan = O1.plan(C.sum(0).tolist(), P)
+    rows = {p: _few_expert_rows(ids_all[p], 12, 16, 8) for p in range(P)}
+    rows_file = os.path.join(tmp_path, "rows.npz")
+    np.savez(rows_file, **{f"r{p}": rows[p] for p in range(P)})
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29591", LLEP_TEST_ROWS=rows_file)
+    cmd = [sys.executable, os.path.join(HERE, "mp_layer_worker.py"), str(P), cfg, "95", "1", str(tmp_path)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = [np.load(os.path.join(tmp_path, f"rank{p}.npz")) for p in range(P)]
+    dp = L.parse_plan(bytes(res[0]["plan"].tobytes()))
+    assert [list(A) for A in dp.chunks] == [list(A) for A in ref_plan.chunks] and len(ref_plan.transfers) > 0
+    LC.check_index_work(res, "llep", ref_plan, ids_all, sh.n_experts)
+    LC.check_index_work(res, "ep", O1.ep_plan(C.sum(0).tolist(), P, 1.0, fallback=False), ids_all, sh.n_experts)
+    w = LC.OracleWeights(sh.d_model, sh.d_ff, 21)
+    for p in range(P):
+        ref = LC.oracle_rank_output(sh, p, ids_all[p], W.gate_weights(sh.tokens_per_rank, sh.top_k, p, 21), 21,
+                                    rows=rows[p], weights=w)
+        mr, l2 = LC.errors(res[p]["llep"].astype(np.float64), ref)
+        assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (p, mr, l2)
+        assert bool(res[p]["same"])

@@ -200,6 +200,7 @@ struct llep_context {
   int32_t *err_host = nullptr;            // mapped pinned
   uint8_t *plan_mirror = nullptr;         // mapped pinned, plan blob bytes
   uint16_t *act = nullptr;                // A [arena_rows, H]
+  int32_t *rtok = nullptr;                // [arena_rows] token of each gathered receive row (a6 local rows)
   size_t scratch_bytes = 0;
   // symmetric arena
   uint8_t *arena = nullptr;
@@ -328,7 +329,7 @@ static ArenaGeometry geometry(const llep_context *c) {
 // every device byte the context holds: arena + scratch + activations + backward buffers + lazily
 // grown backward workspaces
 static size_t held_bytes(const llep_context *c) {
-  return c->arena_bytes + c->scratch_bytes + (size_t)c->arena_rows * c->H * 2 +
+  return c->arena_bytes + c->scratch_bytes + (size_t)c->arena_rows * (c->H * 2 + 4) +
          bwd_local_bytes(c, c->arena_rows, c->arena_foreign) + c->lazy_bytes;
 }
 
@@ -369,7 +370,7 @@ static llep_status alloc_arena(llep_context *c, int64_t rows, int32_t foreign) {
     probe_sizes.backward = c->backward;
     probe_sizes.arena_grad = c->arena_grad;
     layout_offsets(&probe_sizes, rows, foreign);
-    const int64_t need = (int64_t)(probe_sizes.arena_bytes + c->scratch_bytes + (size_t)rows * c->H * 2 +
+    const int64_t need = (int64_t)(probe_sizes.arena_bytes + c->scratch_bytes + (size_t)rows * (c->H * 2 + 4) +
                                    bwd_local_bytes(c, rows, foreign) + c->lazy_bytes);
     if (need > c->mem_cap) {
       set_error("memory cap: the plan needs %.2f GB on this device (arena + activations + scratch), "
@@ -380,6 +381,8 @@ static llep_status alloc_arena(llep_context *c, int64_t rows, int32_t foreign) {
   close_peers(c);
   if (c->arena) cudaFree(c->arena);
   if (c->act) cudaFree(c->act);
+  if (c->rtok) cudaFree(c->rtok);
+  c->rtok = nullptr;
   void *bufs[] = {c->gu, c->da0, c->aw, c->dgu, c->stage13, c->stage2};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -391,6 +394,7 @@ static llep_status alloc_arena(llep_context *c, int64_t rows, int32_t foreign) {
   LLEP_CUDA(cudaMalloc(&c->arena, c->arena_bytes));
   LLEP_CUDA(cudaMemset(c->arena, 0, c->off_x));  // geometry + flags + load matrix
   LLEP_CUDA(cudaMalloc(&c->act, (size_t)rows * c->H * 2));
+  LLEP_CUDA(cudaMalloc(&c->rtok, (size_t)rows * 4));
   if (c->backward) {
     LLEP_CUDA(cudaMalloc(&c->gu, (size_t)rows * 2 * c->H * 2));
     LLEP_CUDA(cudaMalloc(&c->da0, (size_t)rows * c->H * 2));
@@ -546,7 +550,7 @@ void llep_context_destroy(llep_context *c) {
   close_peers(c);
   void *ptrs[] = {c->tile_cnt, c->tile_off, c->cnt, c->local_rank, c->prep_ids, c->slot_dst, c->err,
                   c->lm_local, c->rows_on, c->chunk_row, c->foreign_slot, c->dev_padded,
-                  c->dev_foreign, c->groups, c->sched, c->mblk_src, c->block_done, c->summary, c->d_ptrs, c->act, c->arena,
+                  c->dev_foreign, c->groups, c->sched, c->mblk_src, c->block_done, c->summary, c->d_ptrs, c->act, c->rtok, c->arena,
                   c->gu, c->da0, c->aw, c->dgu, c->stage13, c->stage2, c->wsbuf, c->dotp};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -940,6 +944,16 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   da.peer_flags = overlap ? peer_flags(c) : nullptr;
   da.epoch = aepoch;
   da.block_done = c->block_done;
+  // a6 local rows, opt-in (LLEP_GATHER=1): rows this rank routes to itself, in m-blocks fed by this rank
+  // alone, are gathered by GEMM1 from x with TMA gather4 instead of copied.  Bit-identical, but OFF by
+  // default: gather4 moves ~22 cycles per 128-byte row per SM (1.7 TB/s over 148 SMs, any row order,
+  // profiles/r02_gather4_probe.jsonl), 4x short of what the A operand of a re-used tile needs, so GEMM1
+  // took 10.2 ms instead of 3.6 ms at G120 P=1 to save the 0.18 ms copy
+  const char *gv = getenv("LLEP_GATHER");
+  const bool gather = c->row_align == 256 && gv && atoi(gv) == 1;
+  da.rtok = gather ? c->rtok : nullptr;
+  da.mblk_src = c->mblk_src;
+  da.row_align = c->row_align;
   LLEP_CUDA(launch_dispatch(da, s));
   c->launches += B > 0 || overlap;
   if (!overlap && (st = barrier(c, s)) != LLEP_OK) return st;   // dispatched rows landed
@@ -974,6 +988,10 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   g1.peer_slot = nullptr;
   g1.num_sms = c->num_sms;
   g1.row_align = c->row_align;
+  g1.xg = gather ? x : nullptr;
+  g1.xg_rows = B;
+  g1.rtok = gather ? c->rtok : nullptr;
+  g1.self_mask = 1u << c->rank;
   if (sum.my_groups > 0 && (st = run_grouped_gemm(g1, s)) != LLEP_OK) return st;
   c->launches += sum.my_groups > 0;
   mark(c, 6, s);
@@ -981,6 +999,8 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   GemmArgs g2 = g1;
   g2.mode = 1;
   g2.out2 = nullptr;
+  g2.xg = nullptr;
+  g2.rtok = nullptr;
   g2.a = c->act;
   g2.kdim = H;
   g2.w_native = w2;
@@ -1144,6 +1164,9 @@ static llep_status moe_backward(llep_context *c, const uint16_t *x, const int32_
   da.peer_flags = nullptr;   // the backward keeps its barrier (weights and rows joined before the GEMMs)
   da.epoch = 0;
   da.block_done = c->block_done;
+  da.rtok = nullptr;         // the backward GEMMs read every row from the receive buffer
+  da.mblk_src = nullptr;
+  da.row_align = c->row_align;
   LLEP_CUDA(launch_dispatch(da, s));
   c->launches += B > 0;
   if (any_copy) LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));

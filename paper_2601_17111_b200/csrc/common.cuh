@@ -184,6 +184,12 @@ struct DispatchArgs {
   uint32_t *const *peer_flags;
   uint32_t epoch;
   uint32_t *block_done;
+  // row a6 local-row gather: a row this rank sends to ITSELF, in an m-block whose rows all come from
+  // this rank (mblk_src[row / row_align] == 1 << rank), is not copied: rtok[row] = its token index and
+  // GEMM1 gathers x[t] straight from the caller's tokens with TMA (nullptr: copy every row)
+  int32_t *rtok;
+  const uint32_t *mblk_src;
+  int32_t row_align;
 };
 cudaError_t launch_dispatch(const DispatchArgs &a, cudaStream_t s);
 
@@ -228,6 +234,12 @@ struct GemmArgs {
                              //   peer_slot[rank] + slot*nout (nullptr: write `out` rows)
   int32_t num_sms;
   int32_t row_align;         // 128: 1-CTA M=128 tiles; 256: 2-CTA (cta_group::2) M=256 tiles
+  // modes 0/3, pair tiles: m-blocks with mblk_src[mblk] == self_mask read their A rows straight from
+  // the tokens xg [xg_rows, kdim] (TMA gather4 of rows rtok[row]) instead of a (nullptr: off)
+  const uint16_t *xg;
+  int64_t xg_rows;
+  const int32_t *rtok;
+  uint32_t self_mask;
 };
 llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s);
 

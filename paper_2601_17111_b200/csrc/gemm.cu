@@ -67,6 +67,10 @@ struct GemmParams {
   const int32_t *row_src;
   uint16_t *const *peer_slot;
   __nv_bfloat16 *out2;   // mode 3: raw [g | u] pre-activations, rows of 2 * nout (training forward)
+  CUtensorMap tmXg;      // pair kernel, modes 0/3: the caller's tokens [xg_rows, kdim], {64 x 1} boxes
+  const int32_t *rtok;   //   token row of each receive row of a gathered m-block (nullptr: no gather)
+  int32_t xg_rows;
+  uint32_t self_mask;    //   m-blocks with mblk_src == self_mask (all rows from this rank) are gathered
 };
 
 // Row f2: wait until foreign slot f's weights have landed (flag published by the native device
@@ -499,67 +503,104 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------------------------------------------------------- TMA producer (both CTAs)
-      // L2 policy: a small group's weights are read by one m-block only (evict first) so they do
-      // not push the large groups' re-used weights and activation tiles out of L2
-      const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_normal();
-      const uint64_t pol_act = l2_policy_evict_normal();
-      int stage = 0;
-      uint32_t phase = 0;
-      uint32_t seen = 0;   // sources whose arrival this thread already acquired
-      for (int t = pair; t < total_tiles; t += n_pairs) {
-        TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
-        ti.swap = p.swap && ti.row_end - ti.row0 <= 64;
-        const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
-        const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
-        const int brow = MODE != 1 ? wbase + (int)crank * p.wup_off : wbase + (int)crank * (BN / 2);
+    // ------------------------------------------------------------------ TMA producer (both CTAs)
+    // Lane 0 waits for foreign weights / dispatched rows and issues the box loads; for a gathered
+    // m-block (modes 0/3: every row of it was routed from this rank to itself) all 32 lanes issue
+    // TMA gather4 loads of their 4 token rows of x (the dispatch did not copy them, a6 local rows).
+    // L2 policy: a small group's weights are read by one m-block only (evict first) so they do
+    // not push the large groups' re-used weights and activation tiles out of L2
+    const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_normal();
+    const uint64_t pol_act = l2_policy_evict_normal();
+    const bool gather_on = (MODE == 0 || MODE == 3) && p.rtok != nullptr;
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t seen = 0;   // sources whose arrival lane 0 already acquired
+    for (int t = pair; t < total_tiles; t += n_pairs) {
+      TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
+      ti.swap = p.swap && ti.row_end - ti.row0 <= 64;
+      const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
+      const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
+      const int brow = MODE != 1 ? wbase + (int)crank * p.wup_off : wbase + (int)crank * (BN / 2);
+      if (lane == 0) {
         wait_weights(p, ti.wslot);
         wait_sources(p, ti.mblk, seen);
-        // swapped tile: this CTA's 128 weight rows as the A operand (mode 0/2/3: 64 gate + the
-        // matching 64 up rows of features nb*BNO + crank*64 ...; mode 1: rows nb*BN + crank*BN/2
-        // ...) and its 32 of the group's <= 64 token rows as the B operand
-        const CUtensorMap *wms = ti.wslot >= 0 ? &p.tmW0s : &p.tmW1s;
-        const int srow = MODE != 1 ? wbase + (int)crank * 64 : wbase + (int)crank * (BN / 2);
-        const int srow2 = MODE != 1 ? srow + p.wup_off : srow + 64;
-        if (ti.swap) {
-          for (int kb = 0; kb * SWK * BK < p.kdim; ++kb) {
-            mbar_wait(smem_u32(empty + stage), phase ^ 1);
-            const int nsub = min(SWK, (p.kdim - kb * SWK * BK + BK - 1) / BK);
-            const uint32_t fl = smem_u32(full + stage);
+      }
+      // gathered block: lane l holds the token rows of this CTA's rows base + 4l .. base + 4l + 3
+      // (rows past the group's end read token 0; they are computed on and masked at the store)
+      const bool gat = gather_on && __ldg(p.mblk_src + ti.mblk) == p.self_mask;
+      const int gbase = ti.swap ? ti.row0 + (int)crank * 32 : ti.row0 + (int)crank * (ti.half ? BM / 2 : BM);
+      const int gn = ti.swap ? 8 : 32;   // lanes with rows: 32 rows (swapped B operand) or 128
+      int gi[4] = {0, 0, 0, 0};
+      if (gat && lane < gn) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = gbase + 4 * lane + i;
+          const int tk = r < ti.row_end ? __ldg(p.rtok + r) : 0;
+          gi[i] = (unsigned)tk < (unsigned)p.xg_rows ? tk : 0;
+        }
+      }
+      __syncwarp();
+      // swapped tile: this CTA's 128 weight rows as the A operand (mode 0/2/3: 64 gate + the
+      // matching 64 up rows of features nb*BNO + crank*64 ...; mode 1: rows nb*BN + crank*BN/2
+      // ...) and its 32 of the group's <= 64 token rows as the B operand
+      const CUtensorMap *wms = ti.wslot >= 0 ? &p.tmW0s : &p.tmW1s;
+      const int srow = MODE != 1 ? wbase + (int)crank * 64 : wbase + (int)crank * (BN / 2);
+      const int srow2 = MODE != 1 ? srow + p.wup_off : srow + 64;
+      if (ti.swap) {
+        for (int kb = 0; kb * SWK * BK < p.kdim; ++kb) {
+          mbar_wait(smem_u32(empty + stage), phase ^ 1);
+          const int nsub = min(SWK, (p.kdim - kb * SWK * BK + BK - 1) / BK);
+          const uint32_t fl = smem_u32(full + stage);
+          const uint32_t fb = mapa_shared(fl, 0);
+          if (lane == 0) {
             if (leader) mbar_expect_tx(fl, 2 * nsub * (BM * 128 + 32 * 128));
-            const uint32_t fb = mapa_shared(fl, 0);
             for (int s2 = 0; s2 < nsub; ++s2) {
               const uint32_t ad = s2 < 2 ? smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128))
                                          : smem_u32(sB + stage * C::B_BYTES);
-              const uint32_t bd = smem_u32(sB + stage * C::B_BYTES + (SWK == 3 ? BM * 128 : 0) + s2 * (32 * 128));
               tma_load_2d_pair(ad, wms, fb, (kb * SWK + s2) * BK, srow, ti.small ? pol_first : pol_last);
               tma_load_2d_pair(ad + 64 * 128, wms, fb, (kb * SWK + s2) * BK, srow2, ti.small ? pol_first : pol_last);
-              tma_load_2d_pair(bd, &p.tmAs, fb, (kb * SWK + s2) * BK, ti.row0 + (int)crank * 32, pol_act);
-            }
-            if (++stage == S) {
-              stage = 0;
-              phase ^= 1;
             }
           }
-          continue;
-        }
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(smem_u32(empty + stage), phase ^ 1);
-          const int nsub = min(KSUB, (p.kdim - kb * KST + BK - 1) / BK);   // skip all-OOB sub-tiles
-          const uint32_t fl = smem_u32(full + stage);
-          if (leader) mbar_expect_tx(fl, 2 * nsub * (C::STAGE / KSUB));
-          const uint32_t fb = mapa_shared(fl, 0);
           for (int s2 = 0; s2 < nsub; ++s2) {
-            tma_load_2d_pair(smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128)), &p.tmA, fb,
-                             (kb * KSUB + s2) * BK, ti.row0 + (int)crank * (ti.half ? BM / 2 : BM), pol_act);
-            tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES + s2 * ((BN / 2) * 128)), wm, fb,
-                             (kb * KSUB + s2) * BK, brow, ti.small ? pol_first : pol_last);
+            const uint32_t bd = smem_u32(sB + stage * C::B_BYTES + (SWK == 3 ? BM * 128 : 0) + s2 * (32 * 128));
+            if (!gat) {
+              if (lane == 0) tma_load_2d_pair(bd, &p.tmAs, fb, (kb * SWK + s2) * BK, ti.row0 + (int)crank * 32, pol_act);
+            } else if (lane < gn) {
+              tma_gather4_pair(bd + lane * 512, &p.tmXg, fb, (kb * SWK + s2) * BK, gi[0], gi[1], gi[2], gi[3], pol_act);
+            }
           }
+          __syncwarp();
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
+        }
+        continue;
+      }
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(smem_u32(empty + stage), phase ^ 1);
+        const int nsub = min(KSUB, (p.kdim - kb * KST + BK - 1) / BK);   // skip all-OOB sub-tiles
+        const uint32_t fl = smem_u32(full + stage);
+        const uint32_t fb = mapa_shared(fl, 0);
+        if (lane == 0) {
+          if (leader) mbar_expect_tx(fl, 2 * nsub * (C::STAGE / KSUB));
+          for (int s2 = 0; s2 < nsub; ++s2) {
+            if (!gat)
+              tma_load_2d_pair(smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128)), &p.tmA, fb,
+                               (kb * KSUB + s2) * BK, ti.row0 + (int)crank * (ti.half ? BM / 2 : BM), pol_act);
+            tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES + s2 * ((BN / 2) * 128)), wm, fb,
+                             (kb * KSUB + s2) * BK, brow, ti.small ? pol_first : pol_last);
+          }
+        }
+        if (gat) {
+          for (int s2 = 0; s2 < nsub; ++s2)
+            tma_gather4_pair(smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128)) + lane * 512, &p.tmXg, fb,
+                             (kb * KSUB + s2) * BK, gi[0], gi[1], gi[2], gi[3], pol_act);
+        }
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
@@ -1036,6 +1077,15 @@ llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
                 (int64_t)(g.w_foreign ? g.n_foreign : g.n_native) * wrows, g.kdim, 64)) {
     set_error("cuTensorMapEncodeTiled failed (swapped-tile maps)");
     return LLEP_ERR_CUDA;
+  }
+  if ((MODE == 0 || MODE == 3) && g.rtok && g.xg && g.xg_rows > 0 && g.mblk_src) {
+    if (!make_map(&prm.tmXg, g.xg, g.xg_rows, g.kdim, 1)) {
+      set_error("cuTensorMapEncodeTiled failed (token gather map)");
+      return LLEP_ERR_CUDA;
+    }
+    prm.rtok = g.rtok;
+    prm.xg_rows = (int32_t)g.xg_rows;
+    prm.self_mask = g.self_mask;
   }
   prm.wrows = wrows;
   prm.wup_off = MODE != 1 ? g.nout : 0;

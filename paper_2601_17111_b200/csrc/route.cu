@@ -203,7 +203,7 @@ __device__ __forceinline__ void dispatch_token(const DispatchArgs &a, int64_t t,
   const PlanLayout L = plan_layout(N, P);
   const int32_t *n_chunks = reinterpret_cast<const int32_t *>(plan + L.off_n_chunks);
   const llep_chunk *chunks = reinterpret_cast<const llep_chunk *>(plan + L.off_chunks);
-  int dev = -1, row = 0;
+  int dev = -1, row = 0, gathered = 0;
   if (lane < K) {
     const int64_t j = t * K + lane;
     // The plan, the load matrix and the local ranks all come from llep_prepare's ids, so the slot is
@@ -227,6 +227,11 @@ __device__ __forceinline__ void dispatch_token(const DispatchArgs &a, int64_t t,
     }
     a.slot_dst[2 * j] = changed ? -1 : dev;
     a.slot_dst[2 * j + 1] = row;
+    // local-row gather: GEMM1 reads this row from x[t] itself, nothing to copy
+    if (dev == a.rank && a.rtok && a.mblk_src[row / a.row_align] == (1u << a.rank)) {
+      a.rtok[row] = (int32_t)t;
+      gathered = 1;
+    }
     if (dev >= 0) {
       a.peer_g[dev][row] = changed ? 0.f : a.w[j];
       // (source rank, flat slot) of this receive row: the GEMM2 epilogue pushes the row's output
@@ -235,6 +240,10 @@ __device__ __forceinline__ void dispatch_token(const DispatchArgs &a, int64_t t,
     }
   }
   const int nv = a.D / 8;  // 16-byte vectors per row
+  if (a.rtok) {   // drop the gathered slots from the copy; nothing left to copy -> skip the row load
+    if (gathered) dev = -1;
+    if (!__any_sync(0xffffffffu, dev >= 0)) return;
+  }
   for (int src_i = 0; src_i < (a.x2 ? 2 : 1); ++src_i) {
     const int4 *src = reinterpret_cast<const int4 *>(src_i ? a.x2 : a.x) + t * nv;
     uint16_t *const *peer = src_i ? a.peer_x2 : a.peer_x;

@@ -18,6 +18,9 @@ sys.path.insert(0, HERE)
 
 
 def main():
+    # the check reads the receive buffer: the dispatch must copy every row, including the local rows
+    # GEMM1 would gather straight from x under the opt-in LLEP_GATHER=1 (a6 local rows)
+    os.environ.pop("LLEP_GATHER", None)
     import torch
     import torch.distributed as dist
     import layer_case as LC

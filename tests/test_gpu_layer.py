@@ -517,3 +517,34 @@ def test_f3_dsv3_p4_processes(L, tmp_path):
         mr, l2 = LC.errors(res[p]["llep"].astype(np.float64), ref)
         assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (p, mr, l2)
         assert bool(res[p]["same"])
+
+
+@pytest.mark.parametrize("cfg,pct,nhot", [("tiny", 95, 1), ("tiny", None, 0), ("tiny", 50, 4), ("g20", 95, 1)])
+def test_local_gather_bitwise_equals_copy(L, cfg, pct, nhot):
+    """a6 local rows (opt-in LLEP_GATHER=1): GEMM1 gathering this rank's own rows from x (TMA gather4, no
+    dispatch copy) gives bit-identical outputs and saved [g | u] to the default copy into the receive
+    buffer: same A tiles in shared memory, same MMAs.  Covers full, half and swapped tiles."""
+    base = W.CONFIGS[cfg]
+    B = min(base.tokens_per_rank, 4096)
+    sh = W.LayerShape(base.n_experts, base.top_k, base.d_model, base.d_ff, B, 1)
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, pct, nhot, 13, "cuda")
+    ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, 1, 0, 0, B)
+    res = {}
+    for mode in ("gather", "copy"):
+        if mode == "gather":
+            os.environ["LLEP_GATHER"] = "1"
+        try:
+            plan, req = ctx.prepare(ids)
+            out = ctx.forward(x, ids, gates, w13, w2, plan)
+            gu = torch.zeros((int(req.rows_needed), 2 * sh.d_ff), dtype=torch.bfloat16, device="cuda")
+            out2, gu = ctx.forward_train(x, ids, gates, w13, w2, plan, gu=gu)
+            torch.cuda.synchronize()
+            res[mode] = (out.cpu(), out2.cpu(), gu.cpu())
+        finally:
+            os.environ.pop("LLEP_GATHER", None)
+    for a, b in zip(res["gather"], res["copy"]):
+        assert torch.equal(a, b)
+    ref = LC.oracle_rank_output(sh, 0, ids_np, g_np, 13, rows=np.arange(min(B, 256)))
+    mr, l2 = LC.errors(_to_np(res["gather"][0][: min(B, 256)]), ref)
+    assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (mr, l2)
+    ctx.close()

@@ -234,6 +234,27 @@ llep_status llep_moe_forward_train(llep_context *ctx, const uint16_t *x, const i
                                    const uint16_t *w2, const void *plan, uint16_t *out, uint16_t *gu_save,
                                    int64_t gu_rows, void *stream);
 
+/* llep_moe_layer -- the whole layer of Alg. 4 in ONE stream-ordered call with NO host
+ * synchronisation and no host reads of device data: llep_prepare's kernels (a1 histogram + local
+ * ranks, a2 count push + barrier, a4 device planner into plan_out, a5 layout) followed by
+ * llep_moe_forward's (a7, a6, a8, a9, a10).  The launch sequence depends only on (ctx, n_tokens), so
+ * the call can be captured in a CUDA graph and replayed with new x / topk_ids / topk_w contents: the
+ * plan is recomputed on the device every replay.  Differences from the two-call path:
+ *   - the group count of the GEMMs stays on the device (layout kernel);
+ *   - a7 is issued by the GPU (one small kernel per broadcast-tree level on a side stream, NVLink
+ *     peer stores, release flags per foreign slot) instead of copy engines planned on the host;
+ *   - the arena must already hold the plan (llep_context_reserve beforehand, with every rank's
+ *     rows / foreign slots, e.g. from an earlier llep_prepare's llep_requirements or a bound).  A plan
+ *     that does not fit is detected on the device identically on every rank: that call writes no
+ *     receive rows and computes no tiles (its `out` is undefined) and the next llep_context_check
+ *     returns LLEP_ERR_PLAN.  Other device errors are sticky in the same way.
+ *   - no per-phase timing (llep_context_set_timing covers the two-call path only).
+ * Arguments as llep_prepare + llep_moe_forward (plan_out: device buffer of llep_plan_bytes, written).
+ * Every output equals the two-call path's bit for bit.  Synchronous errors: INVALID, COMM, CUDA. */
+llep_status llep_moe_layer(llep_context *ctx, const uint16_t *x, const int32_t *topk_ids, const float *topk_w,
+                           int64_t n_tokens, const uint16_t *w13, const uint16_t *w2, const llep_params *params,
+                           int32_t force_ep, void *plan_out, uint16_t *out, void *stream);
+
 /* llep_moe_backward -- the backward pass of the layer (row f1) under the plan of
  * llep_prepare for these topk_ids, recomputing the forward internals (nothing is kept from a
  * forward call), for the loss L with dL/dout = dout:

@@ -222,10 +222,10 @@ struct llep_context {
   uint8_t *peer_base[kMaxWorld] = {};
   bool peer_opened[kMaxWorld] = {};
   bool peers_ready = false;
-  void **d_ptrs = nullptr;  // device: flags[P], lm[P], x[P], g[P], o[P], grad[P]
-  uint32_t epoch = 0;
-  uint32_t wepoch = 0;      // row f2: weight-flag epoch, one per forward call (same on every rank)
-  uint32_t aepoch = 0;      // row f2: dispatch-arrival epoch, one per forward call
+  void **d_ptrs = nullptr;  // device: flags[P], lm[P], x[P], g[P], o[P], grad[P], rsrc[P], slot[P], w13[P], w2[P]
+  uint32_t *ep = nullptr;   // device epochs [4] (common.cuh kEp*): barrier, weight flags, dispatch arrivals
+  int32_t *ngroups_dev = nullptr;   // capture-safe layer: this rank's group count (0 on arena overflow)
+  uint32_t *push_cnt = nullptr;     // capture-safe layer: [kMaxPushItems] chunk counts of the GPU weight push
   // host copy of the last prepared plan
   std::vector<uint8_t> plan_host;
   const void *plan_dev_cached = nullptr;
@@ -236,13 +236,14 @@ struct llep_context {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // measurement
   bool timing = false, pending = false;
+  bool in_layer = false;    // inside llep_moe_layer (capture-safe: no phase events, no host reads)
   cudaEvent_t mark[9] = {};
   double phase_ms[LLEP_NUM_PHASES] = {};
   int64_t calls = 0, launches = 0, gemm_rows = 0, pending_rows = 0;
 };
 
 static void mark(llep_context *c, int i, cudaStream_t s) {
-  if (c->timing) cudaEventRecord(c->mark[i], s);
+  if (c->timing && !c->in_layer) cudaEventRecord(c->mark[i], s);
 }
 
 // fold the events of the last completed prepare+forward into the totals
@@ -342,8 +343,10 @@ static void close_peers(llep_context *c) {
   c->peers_ready = false;
 }
 
+constexpr int kPeerPtrArrays = 10;
+
 static llep_status upload_peer_ptrs(llep_context *c) {
-  std::vector<void *> h(8 * c->P);
+  std::vector<void *> h(kPeerPtrArrays * c->P);
   for (int q = 0; q < c->P; ++q) {
     uint8_t *b = c->peer_base[q];
     h[q] = b + c->off_flags;
@@ -354,8 +357,10 @@ static llep_status upload_peer_ptrs(llep_context *c) {
     h[5 * c->P + q] = b + c->off_grad;
     h[6 * c->P + q] = b + c->off_rsrc;
     h[7 * c->P + q] = b + c->off_slot;
+    h[8 * c->P + q] = b + c->off_w13;
+    h[9 * c->P + q] = b + c->off_w2;
   }
-  LLEP_CUDA(cudaMemcpy(c->d_ptrs, h.data(), sizeof(void *) * 8 * c->P, cudaMemcpyHostToDevice));
+  LLEP_CUDA(cudaMemcpy(c->d_ptrs, h.data(), sizeof(void *) * kPeerPtrArrays * c->P, cudaMemcpyHostToDevice));
   return LLEP_OK;
 }
 
@@ -520,7 +525,12 @@ llep_status llep_context_create(const llep_shape *s, int32_t rank, int32_t devic
   if (!e) e = A(&c->block_done, sizeof(uint32_t));
   if (!e) e = cudaMemset(c->block_done, 0, sizeof(uint32_t));
   if (!e) e = A(&c->summary, sizeof(LayoutSummary));
-  if (!e) e = A(&c->d_ptrs, sizeof(void *) * 8 * P);
+  if (!e) e = A(&c->d_ptrs, sizeof(void *) * kPeerPtrArrays * P);
+  if (!e) e = A(&c->ep, sizeof(uint32_t) * 4);
+  if (!e) e = cudaMemset(c->ep, 0, sizeof(uint32_t) * 4);
+  if (!e) e = A(&c->ngroups_dev, sizeof(int32_t));
+  if (!e) e = A(&c->push_cnt, sizeof(uint32_t) * kMaxPushItems);
+  if (!e) e = cudaMemset(c->push_cnt, 0, sizeof(uint32_t) * kMaxPushItems);
   if (!e) e = cudaMemset(c->err, 0, sizeof(int32_t) * 4);
   if (!e) e = cudaHostAlloc(&c->summary_host, sizeof(LayoutSummary), cudaHostAllocMapped);
   if (!e) e = cudaHostAlloc(&c->err_host, sizeof(int32_t) * 4, cudaHostAllocMapped);
@@ -550,7 +560,7 @@ void llep_context_destroy(llep_context *c) {
   close_peers(c);
   void *ptrs[] = {c->tile_cnt, c->tile_off, c->cnt, c->local_rank, c->prep_ids, c->slot_dst, c->err,
                   c->lm_local, c->rows_on, c->chunk_row, c->foreign_slot, c->dev_padded,
-                  c->dev_foreign, c->groups, c->sched, c->mblk_src, c->block_done, c->summary, c->d_ptrs, c->act, c->rtok, c->arena,
+                  c->dev_foreign, c->groups, c->sched, c->mblk_src, c->block_done, c->summary, c->d_ptrs, c->ep, c->ngroups_dev, c->push_cnt, c->act, c->rtok, c->arena,
                   c->gu, c->da0, c->aw, c->dgu, c->stage13, c->stage2, c->wsbuf, c->dotp};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -660,9 +670,8 @@ static float *const *peer_g(llep_context *c) { return reinterpret_cast<float *co
 
 static llep_status barrier(llep_context *c, cudaStream_t s) {
   if (c->P == 1) return LLEP_OK;
-  ++c->epoch;
   ++c->launches;
-  LLEP_CUDA(launch_barrier(peer_flags(c), c->rank, c->P, c->epoch, c->err + 1, s));
+  LLEP_CUDA(launch_barrier(peer_flags(c), c->rank, c->P, c->ep, c->err + 1, s));
   return LLEP_OK;
 }
 
@@ -694,8 +703,12 @@ static void fill_req(llep_context *c, llep_requirements *req) {
   req->n_transfers = s.n_transfers;
 }
 
-static llep_status run_layout(llep_context *c, const void *plan, cudaStream_t s) {
+static llep_status run_layout(llep_context *c, const void *plan, cudaStream_t s, bool layer = false) {
   LayoutArgs la;
+  la.arena_rows = layer ? c->arena_rows : 0;   // the layer call checks the arena fit on the device
+  la.arena_foreign = c->arena_foreign;
+  la.n_groups_dev = layer ? c->ngroups_dev : nullptr;
+  la.err = layer ? c->err : nullptr;
   la.plan = plan;
   la.load_matrix = c->lm_local;
   la.N = c->N;
@@ -719,10 +732,12 @@ static llep_status run_layout(llep_context *c, const void *plan, cudaStream_t s)
 }
 
 // Sticky device error words (err[4]): [0] a router index outside [0, N) (a1); [1] a device barrier (4),
-// weight-flag wait (8) or GEMM weight wait (16) timed out; [2] topk_ids changed between llep_prepare and
-// the forward / backward call (those slots were dropped).  Reported once, then cleared.
+// weight-flag wait (8), GEMM weight wait (16) or source wait (32) timed out, or too many GPU weight pushes
+// (64); [2] topk_ids changed between llep_prepare and the forward / backward call (those slots were
+// dropped); [3] capture-safe layer: the plan did not fit the arena (1) or was inconsistent (2).
+// Reported once, then cleared.
 static llep_status decode_err(llep_context *c, const int32_t *e, cudaStream_t s) {
-  if (!(e[0] | e[1] | e[2])) return LLEP_OK;
+  if (!(e[0] | e[1] | e[2] | e[3])) return LLEP_OK;
   cudaMemsetAsync(c->err, 0, sizeof(int32_t) * 4, s);
   if (e[0]) {
     set_error("router index outside [0, N)");
@@ -731,6 +746,12 @@ static llep_status decode_err(llep_context *c, const int32_t *e, cudaStream_t s)
   if (e[1]) {
     set_error("device barrier or weight-flag wait timed out (a peer did not arrive), code %d", e[1]);
     return LLEP_ERR_COMM;
+  }
+  if (e[3]) {
+    set_error(e[3] & 1 ? "llep_moe_layer: the plan needs more receive rows or foreign-weight slots than the arena "
+                         "holds (llep_context_reserve more); that call computed nothing"
+                       : "llep_moe_layer: plan inconsistent with the load matrix or too many groups");
+    return LLEP_ERR_PLAN;
   }
   set_error("topk_ids changed between llep_prepare and llep_moe_forward/backward: the changed slots were "
             "dropped from that call's output");
@@ -759,21 +780,11 @@ static llep_status read_back(llep_context *c, const void *plan, cudaStream_t s) 
   return LLEP_OK;
 }
 
-llep_status llep_prepare(llep_context *c, const int32_t *ids, int64_t B, const llep_params *prm,
-                         int32_t force_ep, void *plan_out, llep_requirements *req, void *stream) {
-  if (!c || !prm || !plan_out || (B > 0 && !ids)) return invalid("null pointer");
+// a1 -> a2 -> a4 -> a5 on the stream (no host synchronisation): histogram and local ranks, counts
+// pushed into every rank's load matrix + barrier, device planner, layout
+static llep_status prepare_kernels(llep_context *c, const int32_t *ids, int64_t B, const llep_params *prm,
+                                   int32_t force_ep, void *plan_out, cudaStream_t s, bool layer) {
   llep_status st;
-  if ((st = check_params(prm)) != LLEP_OK) return st;
-  if (B < 0 || B > c->max_tokens) return invalid("n_tokens outside [0, max_tokens]");
-  if (c->P > 1 && !c->peers_ready) {
-    set_error("peers not opened (llep_context_open_peers)");
-    return LLEP_ERR_COMM;
-  }
-  cudaStream_t s = (cudaStream_t)stream;
-  collect(c);
-  c->pending = false;
-  c->prepared_tokens = -1;   // a failed prepare leaves nothing for llep_moe_forward to use
-  c->prepared_ids = nullptr;
   const int N = c->N, P = c->P;
   const int64_t slots = B * c->K;
   const int n_tiles = (int)((slots + kTileSlots - 1) / kTileSlots);
@@ -799,8 +810,27 @@ llep_status llep_prepare(llep_context *c, const int32_t *ids, int64_t B, const l
   LLEP_CUDA(launch_planner(c->lm_local, N, P, prm->alpha, prm->min_chunk, prm->lambda, force_ep,
                            plan_out, s));
   ++c->launches;
-  if ((st = run_layout(c, plan_out, s)) != LLEP_OK) return st;
+  if ((st = run_layout(c, plan_out, s, layer)) != LLEP_OK) return st;
   mark(c, 3, s);
+  return LLEP_OK;
+}
+
+llep_status llep_prepare(llep_context *c, const int32_t *ids, int64_t B, const llep_params *prm,
+                         int32_t force_ep, void *plan_out, llep_requirements *req, void *stream) {
+  if (!c || !prm || !plan_out || (B > 0 && !ids)) return invalid("null pointer");
+  llep_status st;
+  if ((st = check_params(prm)) != LLEP_OK) return st;
+  if (B < 0 || B > c->max_tokens) return invalid("n_tokens outside [0, max_tokens]");
+  if (c->P > 1 && !c->peers_ready) {
+    set_error("peers not opened (llep_context_open_peers)");
+    return LLEP_ERR_COMM;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  collect(c);
+  c->pending = false;
+  c->prepared_tokens = -1;   // a failed prepare leaves nothing for llep_moe_forward to use
+  c->prepared_ids = nullptr;
+  if ((st = prepare_kernels(c, ids, B, prm, force_ep, plan_out, s, false)) != LLEP_OK) return st;
   if ((st = read_back(c, plan_out, s)) != LLEP_OK) return st;
   c->prepared_tokens = B;
   c->prepared_ids = ids;
@@ -815,7 +845,7 @@ llep_status llep_prepare(llep_context *c, const int32_t *ids, int64_t B, const l
 // flag; every copy is followed by a release-signal of the destination slot's flag (epoch `ep`).
 // f(e, d) = position of e among d's foreign experts (ascending id).  Side stream, copy engines.
 static llep_status push_weights(llep_context *c, const uint16_t *w13, const uint16_t *w2, cudaStream_t s,
-                                bool *any_copy, uint32_t ep) {
+                                bool *any_copy) {
   const int N = c->N, P = c->P, M = c->M, D = c->D, H = c->H;
   const PlanLayout L = plan_layout(N, P);
   const uint8_t *replica = c->plan_host.data() + L.off_replica;
@@ -853,7 +883,7 @@ static llep_status push_weights(llep_context *c, const uint16_t *w13, const uint
     } else {
       const int f = fslot[(size_t)e * P + c->rank];
       const uint32_t *own = reinterpret_cast<const uint32_t *>(c->arena + c->off_flags) + kWeightFlag0 + f;
-      LLEP_CUDA(launch_wait_flag(own, ep, c->err + 1, c->side));
+      LLEP_CUDA(launch_wait_flag(own, c->ep, c->err + 1, c->side));
       ++c->launches;
       src13 = c->arena + c->off_w13 + (size_t)f * w13_bytes;
       src2 = c->arena + c->off_w2 + (size_t)f * w2_bytes;
@@ -866,17 +896,21 @@ static llep_status push_weights(llep_context *c, const uint16_t *w13, const uint
       LLEP_CUDA(cudaMemcpyAsync(c->peer_base[d] + c->off_w2 + (size_t)f * w2_bytes, src2, w2_bytes,
                                 cudaMemcpyDeviceToDevice, c->side));
       uint32_t *flag = reinterpret_cast<uint32_t *>(c->peer_base[d] + c->off_flags) + kWeightFlag0 + f;
-      LLEP_CUDA(launch_signal(flag, ep, c->side));
+      LLEP_CUDA(launch_signal(flag, c->ep, c->side));
       ++c->launches;
     }
   }
   return LLEP_OK;
 }
 
+// The forward kernels (a7, a6, a8, a9, a10).  layer = false: the two-call path, planned on the host copy
+// of the plan (group count, arena check, copy-engine weight pushes).  layer = true (llep_moe_layer): the
+// plan never leaves the device -- group count from the layout kernel, arena fit checked there, weight
+// pushes issued by the GPU -- so the call is capture-safe.
 static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t *ids,
                                const float *topk_w, int64_t B, const uint16_t *w13,
                                const uint16_t *w2, const void *plan, uint16_t *out, uint16_t *gu_save,
-                               int64_t gu_rows, void *stream) {
+                               int64_t gu_rows, void *stream, bool layer = false) {
   if (!c || !plan || !w13 || !w2 || (B > 0 && (!x || !ids || !topk_w || !out)))
     return invalid("null pointer");
   if (B != c->prepared_tokens) return invalid("n_tokens differs from the last llep_prepare");
@@ -887,12 +921,14 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   }
   cudaStream_t s = (cudaStream_t)stream;
   llep_status st;
-  if (plan != c->plan_dev_cached) {
+  if (!layer && plan != c->plan_dev_cached) {
     if ((st = run_layout(c, plan, s)) != LLEP_OK) return st;
     if ((st = read_back(c, plan, s)) != LLEP_OK) return st;
   }
-  const LayoutSummary &sum = *c->summary_host;
-  if (sum.rows_needed > c->arena_rows || sum.foreign_needed > c->arena_foreign) {
+  LayoutSummary sum_dev_planned;
+  memset(&sum_dev_planned, 0, sizeof(sum_dev_planned));
+  const LayoutSummary &sum = layer ? sum_dev_planned : *c->summary_host;
+  if (!layer && (sum.rows_needed > c->arena_rows || sum.foreign_needed > c->arena_foreign)) {
     set_error("plan needs %lld rows / %d foreign experts, arena holds %lld / %d: call "
               "llep_context_reserve", (long long)sum.rows_needed, sum.foreign_needed,
               (long long)c->arena_rows, c->arena_foreign);
@@ -908,8 +944,41 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   // a7: weight migration, pushed by the native device on a side stream (copy engines); row f2: each
   // destination's GEMM waits for a foreign slot's flag only when it reaches that slot's tiles
   bool any_copy = false;
-  const uint32_t wepoch = ++c->wepoch;
-  if ((st = push_weights(c, w13, w2, s, &any_copy, wepoch)) != LLEP_OK) return st;
+  if (P > 1) {   // this call's weight-flag and arrival epochs (device-resident, same on every rank)
+    LLEP_CUDA(launch_advance(c->ep, s));
+    ++c->launches;
+  }
+  if (!layer) {
+    if ((st = push_weights(c, w13, w2, s, &any_copy)) != LLEP_OK) return st;
+  } else if (P > 1) {
+    // a7 issued by the GPU from the device plan: one launch per broadcast-tree level on the side stream
+    LLEP_CUDA(cudaEventRecord(c->ev_fork, s));
+    LLEP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    any_copy = true;
+    PushArgs pa;
+    pa.plan = plan;
+    pa.foreign_slot = c->foreign_slot;
+    pa.N = N;
+    pa.P = P;
+    pa.M = M;
+    pa.rank = c->rank;
+    pa.w13 = w13;
+    pa.w2 = w2;
+    pa.peer_w13 = reinterpret_cast<uint8_t *const *>(c->d_ptrs + 8 * P);
+    pa.peer_w2 = reinterpret_cast<uint8_t *const *>(c->d_ptrs + 9 * P);
+    pa.peer_flags = peer_flags(c);
+    pa.w13_bytes = (int64_t)2 * H * D * 2;
+    pa.w2_bytes = (int64_t)D * H * 2;
+    pa.ep = c->ep;
+    pa.counters = c->push_cnt;
+    pa.err = c->err;
+    pa.skip = &c->summary->error;
+    for (int lvl = 0; (1 << lvl) < P; ++lvl) {
+      pa.level = lvl;
+      LLEP_CUDA(launch_push_level(pa, c->side));
+      ++c->launches;
+    }
+  }
   mark(c, 4, s);
   if (any_copy) LLEP_CUDA(cudaEventRecord(c->ev_join, c->side));
   // a6: dispatch (gather-on-send into every destination's receive rows)
@@ -940,10 +1009,10 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   // for the sources of that block's rows (and, per foreign group, for its weight flag), so tiles start
   // as their inputs land instead of after the slowest rank (LLEP_DISPATCH_BARRIER=1: old barrier)
   const bool overlap = P > 1 && !getenv("LLEP_DISPATCH_BARRIER");
-  const uint32_t aepoch = ++c->aepoch;
   da.peer_flags = overlap ? peer_flags(c) : nullptr;
-  da.epoch = aepoch;
+  da.ep = c->ep;
   da.block_done = c->block_done;
+  da.skip = layer ? &c->summary->error : nullptr;   // arena overflow: store nothing (flags still go out)
   // a6 local rows, opt-in (LLEP_GATHER=1): rows this rank routes to itself, in m-blocks fed by this rank
   // alone, are gathered by GEMM1 from x with TMA gather4 instead of copied.  Bit-identical, but OFF by
   // default: gather4 moves ~22 cycles per 128-byte row per SM (1.7 TB/s over 148 SMs, any row order,
@@ -974,15 +1043,14 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   g1.nout = H;
   g1.groups = c->groups;
   g1.sched = getenv("LLEP_GEMM_GROUP_ORDER") ? nullptr : c->sched;
-  g1.n_groups_dev = nullptr;
+  g1.n_groups_dev = layer ? c->ngroups_dev : nullptr;   // layer: the count never leaves the device
   g1.n_groups_host = sum.my_groups;
   g1.gate = nullptr;
   g1.out = c->act;
   g1.wflags = P > 1 ? reinterpret_cast<const uint32_t *>(c->arena + c->off_flags) + kWeightFlag0 : nullptr;
-  g1.wepoch = wepoch;
+  g1.ep = c->ep;
   g1.err = c->err;
   g1.arrive = overlap ? reinterpret_cast<const uint32_t *>(c->arena + c->off_flags) + kArriveFlag0 : nullptr;
-  g1.aepoch = aepoch;
   g1.mblk_src = c->mblk_src;
   g1.row_src = nullptr;
   g1.peer_slot = nullptr;
@@ -992,8 +1060,9 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   g1.xg_rows = B;
   g1.rtok = gather ? c->rtok : nullptr;
   g1.self_mask = 1u << c->rank;
-  if (sum.my_groups > 0 && (st = run_grouped_gemm(g1, s)) != LLEP_OK) return st;
-  c->launches += sum.my_groups > 0;
+  const bool gemms = layer || sum.my_groups > 0;
+  if (gemms && (st = run_grouped_gemm(g1, s)) != LLEP_OK) return st;
+  c->launches += gemms;
   mark(c, 6, s);
   // a9: GEMM2 + gate   A [rows, H] -> Y [rows, D]  (Y reuses X's rows: X is dead after GEMM1)
   GemmArgs g2 = g1;
@@ -1012,8 +1081,8 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   // peer stores for remote rows, overlapped with the MMAs of later tiles)
   g2.row_src = reinterpret_cast<const int32_t *>(c->arena + c->off_rsrc);
   g2.peer_slot = reinterpret_cast<uint16_t *const *>(c->d_ptrs + 7 * P);
-  if (sum.my_groups > 0 && (st = run_grouped_gemm(g2, s)) != LLEP_OK) return st;
-  c->launches += sum.my_groups > 0;
+  if (gemms && (st = run_grouped_gemm(g2, s)) != LLEP_OK) return st;
+  c->launches += gemms;
   mark(c, 7, s);
   if ((st = barrier(c, s)) != LLEP_OK) return st;
   // a10: local K-sum of the slot buffer the GEMM2 epilogues (this rank's and every peer's) filled
@@ -1022,11 +1091,38 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   c->launches += B > 0;
   if (any_copy) LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));   // keep the side stream joined
   mark(c, 8, s);
-  if (c->timing) {
+  if (c->timing && !layer) {
     c->pending = true;
     c->pending_rows = sum.my_rows;
   }
   return LLEP_OK;
+}
+
+llep_status llep_moe_layer(llep_context *c, const uint16_t *x, const int32_t *ids, const float *topk_w,
+                           int64_t B, const uint16_t *w13, const uint16_t *w2, const llep_params *prm,
+                           int32_t force_ep, void *plan_out, uint16_t *out, void *stream) {
+  if (!c || !prm || !plan_out || !w13 || !w2 || (B > 0 && (!x || !ids || !topk_w || !out)))
+    return invalid("null pointer");
+  llep_status st;
+  if ((st = check_params(prm)) != LLEP_OK) return st;
+  if (B < 0 || B > c->max_tokens) return invalid("n_tokens outside [0, max_tokens]");
+  if (c->P > 1 && !c->peers_ready) {
+    set_error("peers not opened (llep_context_open_peers)");
+    return LLEP_ERR_COMM;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  c->in_layer = true;   // (pending phase events of an earlier two-call forward stay pending)
+  st = prepare_kernels(c, ids, B, prm, force_ep, plan_out, s, true);
+  if (st == LLEP_OK) {
+    c->prepared_tokens = B;
+    c->prepared_ids = ids;
+    st = moe_forward(c, x, ids, topk_w, B, w13, w2, plan_out, out, nullptr, 0, stream, true);
+  }
+  // the host copy of the plan (plan_host / summary_host) is not this call's: a later llep_moe_forward or
+  // llep_moe_backward re-reads the plan it is given
+  c->plan_dev_cached = nullptr;
+  c->in_layer = false;
+  return st;
 }
 
 
@@ -1137,7 +1233,11 @@ static llep_status moe_backward(llep_context *c, const uint16_t *x, const int32_
   float *G = reinterpret_cast<float *>(c->arena + c->off_g);
   // a7 + a6: weights to the replicas, x and dout rows + gates to their destinations
   bool any_copy = false;
-  if ((st = push_weights(c, w13, w2, s, &any_copy, ++c->wepoch)) != LLEP_OK) return st;
+  if (P > 1) {
+    LLEP_CUDA(launch_advance(c->ep, s));
+    ++c->launches;
+  }
+  if ((st = push_weights(c, w13, w2, s, &any_copy)) != LLEP_OK) return st;
   if (any_copy) LLEP_CUDA(cudaEventRecord(c->ev_join, c->side));
   DispatchArgs da;
   da.x = x;
@@ -1162,7 +1262,8 @@ static llep_status moe_backward(llep_context *c, const uint16_t *x, const int32_
   da.peer_x2 = reinterpret_cast<uint16_t *const *>(c->d_ptrs + 4 * P);
   da.peer_rsrc = nullptr;
   da.peer_flags = nullptr;   // the backward keeps its barrier (weights and rows joined before the GEMMs)
-  da.epoch = 0;
+  da.ep = c->ep;
+  da.skip = nullptr;
   da.block_done = c->block_done;
   da.rtok = nullptr;         // the backward GEMMs read every row from the receive buffer
   da.mblk_src = nullptr;

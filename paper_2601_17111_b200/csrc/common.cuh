@@ -123,7 +123,20 @@ struct LayoutArgs {
   int32_t row_align;           // group row bases / GEMM M tile: 128 or 256
   uint32_t *mblk_src;          // [sched_cap] per m-block (group order) of this rank: bit q set iff the
                                // block holds rows dispatched by source rank q (row f2 arrival waits)
+  // capture-safe layer (llep_moe_layer) only: the arena this call must fit.  A plan that needs more rows
+  // or foreign slots on ANY device (the same decision on every rank) sets summary->error |= 16,
+  // err[3] |= 1 and *n_groups_dev = 0, so no kernel of that call writes past the arena.
+  int64_t arena_rows;          // 0: no check (the two-call path checks on the host)
+  int32_t arena_foreign;
+  int32_t *n_groups_dev;       // this rank's group count for the GEMMs (0 on overflow)
+  int32_t *err;
 };
+
+// Device-resident epochs (one word each, zero at context creation).  Every synchronising kernel reads
+// its epoch from here instead of a launch argument, so a captured CUDA graph replays correctly: the
+// barrier kernel advances kEpBarrier itself; advance_kernel bumps kEpWeight and kEpArrive once at the
+// start of every forward / backward call (P > 1).  All ranks run the same sequence -> same values.
+constexpr int kEpBarrier = 0, kEpWeight = 1, kEpArrive = 2;
 
 // kernel launchers (route.cu / plan.cu / gemm.cu)
 cudaError_t launch_tile_count(const int32_t *ids, int64_t n_slots, int32_t N, int32_t *tile_cnt,
@@ -134,8 +147,9 @@ cudaError_t launch_local_rank(const int32_t *ids, int64_t n_slots, int32_t N, co
                               int32_t *local_rank, int32_t *prep_ids, cudaStream_t s);
 cudaError_t launch_push_counts(const int32_t *cnt, int32_t N, int32_t rank, int32_t P,
                                int32_t *const *peer_lm, cudaStream_t s);
-cudaError_t launch_barrier(uint32_t *const *peer_flags, int32_t rank, int32_t P, uint32_t epoch,
+cudaError_t launch_barrier(uint32_t *const *peer_flags, int32_t rank, int32_t P, uint32_t *ep,
                            int32_t *err, cudaStream_t s);
+cudaError_t launch_advance(uint32_t *ep, cudaStream_t s);
 cudaError_t launch_planner(const int32_t *load_matrix, int32_t N, int32_t P, double alpha,
                            int64_t min_chunk, double lambda, int32_t force_ep, void *plan,
                            cudaStream_t s);
@@ -148,12 +162,12 @@ cudaError_t launch_bwd_swiglu(const Group *groups, int n_groups, int n_rows_tota
                               const uint16_t *dA0, float *gate_io, uint16_t *Aw, uint16_t *dGU, cudaStream_t s);
 cudaError_t launch_grad_reduce(float *dst, const float *base, int n_src, int64_t stride_floats, int64_t n_floats,
                                cudaStream_t s);
-cudaError_t launch_signal(uint32_t *flag, uint32_t v, cudaStream_t s);
-cudaError_t launch_wait_flag(const uint32_t *flag, uint32_t v, int32_t *err, cudaStream_t s);
+cudaError_t launch_signal(uint32_t *flag, const uint32_t *ep, cudaStream_t s);
+cudaError_t launch_wait_flag(const uint32_t *flag, const uint32_t *ep, int32_t *err, cudaStream_t s);
 constexpr int kWeightFlag0 = 32;   // arena flag words: [0, 32) barrier, [32, 32 + kMaxGroups) weight slots,
 constexpr int kArriveFlag0 = kWeightFlag0 + kMaxGroups;   // then [32) dispatch arrivals (one per source)
 constexpr int kFlagWords = kArriveFlag0 + kMaxWorld;
-cudaError_t launch_arrive(uint32_t *const *peer_flags, int32_t rank, int32_t P, uint32_t epoch, cudaStream_t s);
+cudaError_t launch_arrive(uint32_t *const *peer_flags, int32_t rank, int32_t P, const uint32_t *ep, cudaStream_t s);
 cudaError_t launch_combine_local(const uint16_t *slotbuf, int64_t B, int K, int D, const int32_t *slot_dst,
                                  uint16_t *out, cudaStream_t s);
 cudaError_t launch_mirror(const void *plan, size_t plan_bytes, const void *summary, size_t sum_bytes,
@@ -182,8 +196,10 @@ struct DispatchArgs {
   // publishes `epoch` into arrival flag [rank] of every device (release, system scope) once all of this
   // rank's rows are stored; block_done counts finished blocks (rank-local, returns to 0)
   uint32_t *const *peer_flags;
-  uint32_t epoch;
+  const uint32_t *ep;       // device epochs: the arrival value is ep[kEpArrive]
   uint32_t *block_done;
+  const int32_t *skip;      // capture-safe layer: nonzero (arena overflow, LayoutSummary.error bit 16)
+                            // -> the kernel stores nothing but still publishes its arrival flags
   // row a6 local-row gather: a row this rank sends to ITSELF, in an m-block whose rows all come from
   // this rank (mblk_src[row / row_align] == 1 << rank), is not copied: rtok[row] = its token index and
   // GEMM1 gathers x[t] straight from the caller's tokens with TMA (nullptr: copy every row)
@@ -222,12 +238,12 @@ struct GemmArgs {
   const float *gate;         // [rows] (mode 1)
   uint16_t *out;             // [rows, nout]
   uint16_t *out2;            // mode 3 (GEMM1 + SwiGLU that also saves [g | u]): [rows, 2*nout]
-  const uint32_t *wflags;    // row f2: foreign slot f's weights landed when wflags[f] >= wepoch
-  uint32_t wepoch;           //         (nullptr: weights already resident)
+  const uint32_t *wflags;    // row f2: foreign slot f's weights landed when wflags[f] >= ep[kEpWeight]
+  const uint32_t *ep;        //         (nullptr: weights already resident); device epochs
   int32_t *err;              //         err[1] |= 16 if a weight wait times out (~20 s); waits are
                              //         skipped once err[1] is set (a peer failed: no hang)
   const uint32_t *arrive;    // row f2: this rank's dispatch arrival flags [P] (nullptr: rows resident)
-  uint32_t aepoch;           //         source q's rows landed when arrive[q] >= aepoch
+                             //         source q's rows landed when arrive[q] >= ep[kEpArrive]
   const uint32_t *mblk_src;  //         per m-block (group order): mask of the sources of its rows
   const int32_t *row_src;    // mode 1 push epilogue: (slot << 5) | rank of each receive row, and
   uint16_t *const *peer_slot;//   [P] slot buffers [B*K, nout]: the row's output goes to
@@ -242,6 +258,29 @@ struct GemmArgs {
   uint32_t self_mask;
 };
 llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s);
+
+// a7 weight migration issued by the GPU (capture-safe layer): one launch per level of the binomial
+// broadcast tree of every replicated expert (holders h_0 = native, then the replicas ascending; holder i
+// sends to i + 2^t for 2^t > i).  Level 0 = the native sends, level l >= 1 = forwards by holders
+// 2^(l-1) <= i < 2^l, each after acquiring its own slot's flag.  Every launch enumerates this rank's
+// sends of its level from the plan, splits them into chunks over a fixed grid (16-byte loads, NVLink
+// peer stores), and the last chunk of a send releases the destination slot's weight flag.
+struct PushArgs {
+  const void *plan;
+  const int32_t *foreign_slot;      // [N*P] layout: position of e among d's foreign experts, -1 if none
+  int32_t N, P, M, rank, level;
+  const uint16_t *w13, *w2;         // this rank's native weights [M][2H][D], [M][D][H]
+  uint8_t *const *peer_w13;         // [P] foreign-weight regions of every arena (w13 slots, then w2)
+  uint8_t *const *peer_w2;
+  uint32_t *const *peer_flags;      // [P] flag words of every arena
+  int64_t w13_bytes, w2_bytes;      // per expert
+  const uint32_t *ep;               // ep[kEpWeight]: the release value
+  uint32_t *counters;               // [kMaxPushItems] chunk completion counts (return to 0)
+  int32_t *err;                     // err[1] |= 8 when a forward's wait times out
+  const int32_t *skip;              // arena overflow: no pushes (every rank decides the same)
+};
+constexpr int kMaxPushItems = 4096;
+cudaError_t launch_push_level(const PushArgs &a, cudaStream_t s);
 
 // backward GEMMs (gemm.cu).  kind 0: out[r] = a[r, 0:kdim] · W_e[kdim, nout] (bf16 out, grouped by rows,
 // Group.mblk_start counted in units of mblk_scale 128-row blocks); kind 1: out[e] = a[rows_e]ᵀ · b[rows_e]

@@ -59,10 +59,9 @@ struct GemmParams {
   const float *gate;
   __nv_bfloat16 *out;
   const uint32_t *wflags;
-  uint32_t wepoch;
+  const uint32_t *ep;    // device epochs (common.cuh): weights landed at ep[kEpWeight], rows at ep[kEpArrive]
   int32_t *err;
   const uint32_t *arrive;
-  uint32_t aepoch;
   const uint32_t *mblk_src;
   const int32_t *row_src;
   uint16_t *const *peer_slot;
@@ -78,7 +77,7 @@ struct GemmParams {
 // Bounded like the device barriers: after ~20 s (or once another wait / barrier of this rank has
 // failed, err[1] != 0) it gives up and flags err[1] |= 16 (LLEP_ERR_COMM at the next check), so a peer
 // that returned early cannot hang this GPU.
-__device__ __forceinline__ void wait_weights(const GemmParams &p, int wslot) {
+__device__ __forceinline__ void wait_weights(const GemmParams &p, int wslot, uint32_t wepoch) {
   if (wslot >= 0 || !p.wflags) return;
   const uint32_t *f = p.wflags + (-1 - wslot);
   uint32_t v;
@@ -86,7 +85,7 @@ __device__ __forceinline__ void wait_weights(const GemmParams &p, int wslot) {
   long long spins = 0;
   while (true) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-    if ((int32_t)(v - p.wepoch) >= 0) break;
+    if ((int32_t)(v - wepoch) >= 0) break;
     if (((++spins) & 255) == 0) {
       if (p.err && *reinterpret_cast<volatile int32_t *>(p.err + 1) != 0) break;
       if (clock64() - t0 > 40000000000LL) {
@@ -102,7 +101,7 @@ __device__ __forceinline__ void wait_weights(const GemmParams &p, int wslot) {
 // activation rows, wait until every source rank that dispatched rows into that block has published
 // its arrival flag (release after all its rows were stored, route.cu dispatch_kernel), then order the
 // async-proxy (TMA) reads after the acquire.  Bounded like wait_weights.
-__device__ __forceinline__ void wait_sources(const GemmParams &p, int mblk, uint32_t &seen) {
+__device__ __forceinline__ void wait_sources(const GemmParams &p, int mblk, uint32_t &seen, uint32_t aepoch) {
   if (!p.arrive) return;
   uint32_t need = p.mblk_src[mblk] & ~seen;
   if (!need) return;
@@ -112,7 +111,7 @@ __device__ __forceinline__ void wait_sources(const GemmParams &p, int mblk, uint
     const int q = __ffs(need) - 1;
     uint32_t v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p.arrive + q) : "memory");
-    if ((int32_t)(v - p.aepoch) >= 0) {
+    if ((int32_t)(v - aepoch) >= 0) {
       need &= need - 1;
       seen |= 1u << q;
       continue;
@@ -246,12 +245,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
       int stage = 0;
       uint32_t phase = 0;
       uint32_t seen = 0;   // sources whose arrival this thread already acquired
+      const uint32_t wep = p.ep ? p.ep[kEpWeight] : 0u, aep = p.ep ? p.ep[kEpArrive] : 0u;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         const TileInfo ti = decode_tile(t, p.n_ntiles, s_mblk, n_groups, p.groups, p.sched);
         const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
         const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
-        wait_weights(p, ti.wslot);
-        wait_sources(p, ti.mblk, seen);
+        wait_weights(p, ti.wslot, wep);
+        wait_sources(p, ti.mblk, seen, aep);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const uint32_t fb = smem_u32(full + stage);
@@ -515,6 +515,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
     int stage = 0;
     uint32_t phase = 0;
     uint32_t seen = 0;   // sources whose arrival lane 0 already acquired
+    const uint32_t wep = p.ep ? p.ep[kEpWeight] : 0u, aep = p.ep ? p.ep[kEpArrive] : 0u;
     for (int t = pair; t < total_tiles; t += n_pairs) {
       TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
       ti.swap = p.swap && ti.row_end - ti.row0 <= 64;
@@ -522,8 +523,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       const int wbase = (ti.wslot >= 0 ? ti.wslot : (-1 - ti.wslot)) * p.wrows + ti.nb * BNO;
       const int brow = MODE != 1 ? wbase + (int)crank * p.wup_off : wbase + (int)crank * (BN / 2);
       if (lane == 0) {
-        wait_weights(p, ti.wslot);
-        wait_sources(p, ti.mblk, seen);
+        wait_weights(p, ti.wslot, wep);
+        wait_sources(p, ti.mblk, seen, aep);
       }
       // gathered block: lane l holds the token rows of this CTA's rows base + 4l .. base + 4l + 3
       // (rows past the group's end read token 0; they are computed on and masked at the store)
@@ -2119,10 +2120,9 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   prm.groups = g.groups;
   prm.sched = g.sched;
   prm.wflags = g.wflags;
-  prm.wepoch = g.wepoch;
+  prm.ep = g.ep;
   prm.err = g.err;
   prm.arrive = g.arrive;
-  prm.aepoch = g.aepoch;
   prm.mblk_src = g.mblk_src;
   prm.row_src = g.row_src;
   prm.peer_slot = g.peer_slot;

@@ -454,8 +454,12 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(LayoutArgs a) {
     s.force_count = hdr->force_count;
     s.n_transfers = hdr->n_transfers;
     s.error = sm_err | (sm_groups > kMaxGroups ? 2 : 0) | (sm_mblocks > a.sched_cap ? 8 : 0);
+    // capture-safe layer: the arena this call runs in must hold every device's rows (same on all ranks)
+    if (a.arena_rows > 0 && (mx > a.arena_rows || mf > a.arena_foreign)) s.error |= 16;
     s.pad = 0;
     *a.summary = s;
+    if (a.n_groups_dev) *a.n_groups_dev = s.error ? 0 : sm_groups;
+    if (a.err && s.error) atomicOr(a.err + 3, (s.error & 16) ? 1 : 2);
   }
 }
 

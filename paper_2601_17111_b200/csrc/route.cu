@@ -146,8 +146,9 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
 // release (stream order + cumulativity), so after the acquire every peer's earlier stores to
 // this rank's arena are visible to the kernels that follow.  Bounded spin -> COMM error.
 __global__ void barrier_kernel(uint32_t *const *__restrict__ peer_flags, int rank, int P,
-                               uint32_t epoch, int32_t *__restrict__ err) {
+                               uint32_t *__restrict__ ep, int32_t *__restrict__ err) {
   const int q = threadIdx.x;
+  const uint32_t epoch = ep[kEpBarrier] + 1;   // this barrier's epoch (device-resident, see common.cuh)
   if (q < P) {
     __threadfence_system();
     st_release_sys(peer_flags[q] + rank, epoch);
@@ -161,6 +162,13 @@ __global__ void barrier_kernel(uint32_t *const *__restrict__ peer_flags, int ran
       }
     }
   }
+  __syncwarp();
+  if (q == 0) ep[kEpBarrier] = epoch;
+}
+
+__global__ void advance_kernel(uint32_t *ep) {
+  ep[kEpWeight] += 1;
+  ep[kEpArrive] += 1;
 }
 
 // ----------------------------------------------------------------------------- a6: dispatch
@@ -177,7 +185,7 @@ __device__ __forceinline__ void dispatch_token(const DispatchArgs &a, int64_t t,
 __global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_kernel(DispatchArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * kDispatchWarps + (threadIdx.x >> 5);
-  if (t < a.B) dispatch_token(a, t, lane);
+  if (t < a.B && !(a.skip && *a.skip)) dispatch_token(a, t, lane);
   if (!a.peer_flags) return;
   asm volatile("fence.acq_rel.sys;" ::: "memory");
   __syncthreads();
@@ -186,14 +194,16 @@ __global__ void __launch_bounds__(kDispatchWarps * 32) dispatch_kernel(DispatchA
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.block_done) : "memory");
     if (prev == gridDim.x - 1) {
       *a.block_done = 0;   // next call's count (stream-ordered after this kernel)
-      for (int q = 0; q < a.P; ++q) st_release_sys(a.peer_flags[q] + kArriveFlag0 + a.rank, a.epoch);
+      const uint32_t epoch = a.ep[kEpArrive];
+      for (int q = 0; q < a.P; ++q) st_release_sys(a.peer_flags[q] + kArriveFlag0 + a.rank, epoch);
     }
   }
 }
 
 // P=1 or a rank without tokens: publish the arrival flags alone
-__global__ void arrive_kernel(uint32_t *const *__restrict__ peer_flags, int rank, int P, uint32_t epoch) {
+__global__ void arrive_kernel(uint32_t *const *__restrict__ peer_flags, int rank, int P, const uint32_t *ep) {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
+  const uint32_t epoch = ep[kEpArrive];
   for (int q = threadIdx.x; q < P; q += blockDim.x) st_release_sys(peer_flags[q] + kArriveFlag0 + rank, epoch);
 }
 
@@ -447,13 +457,14 @@ __global__ void grad_reduce_kernel(float *__restrict__ dst, const float *__restr
 // Row f2: after the copy engine has written an expert's weights into a peer's foreign slot (same
 // stream, so the copy completed first), publish `v` in that peer's weight flag with release
 // semantics at system scope; the peer's GEMM producers acquire it before loading those weights.
-__global__ void signal_kernel(uint32_t *flag, uint32_t v) {
+__global__ void signal_kernel(uint32_t *flag, const uint32_t *ep) {
   __threadfence_system();
-  st_release_sys(flag, v);
+  st_release_sys(flag, ep[kEpWeight]);
 }
 
 // Row f2 broadcast tree: a replica forwards an expert's weights only after its own copy landed.
-__global__ void wait_flag_kernel(const uint32_t *flag, uint32_t v, int32_t *err) {
+__global__ void wait_flag_kernel(const uint32_t *flag, const uint32_t *ep, int32_t *err) {
+  const uint32_t v = ep[kEpWeight];
   const long long t0 = clock64();
   long long spins = 0;
   while ((int32_t)(ld_acquire_sys(flag) - v) < 0) {
@@ -463,6 +474,133 @@ __global__ void wait_flag_kernel(const uint32_t *flag, uint32_t v, int32_t *err)
     }
   }
   __threadfence_system();
+}
+
+// ------------------------------------------------------------------ a7 issued by the GPU (layer call)
+// One launch per broadcast-tree level (PushArgs in common.cuh).  Items (expert, destination) of this
+// rank's level are enumerated from the plan's replica bytes by warp 0 (ascending expert, then tree
+// step); units = items x 2 MB chunks of the expert's [W13 | W2] bytes, spread over a fixed grid.
+// Deadlock freedom: a level-l forward waits only for sends of lower levels, which other ranks issue
+// from earlier launches of their side stream (each launch finishes before the next starts), and the
+// grid is small (no shared memory beyond 16 KB, 256 threads) so it stays resident beside the GEMMs.
+constexpr int kPushThreads = 256, kPushBlocks = 64;
+constexpr int64_t kPushChunk = int64_t(1) << 21;
+
+__device__ __forceinline__ int tree_holder(int native, uint32_t mask, int i) {
+  if (i == 0) return native;
+  uint32_t m = mask;
+  for (int j = 1; j < i; ++j) m &= m - 1u;   // drop the i-1 lowest replicas
+  return __ffs(m) - 1;
+}
+
+__global__ void __launch_bounds__(kPushThreads) push_level_kernel(PushArgs a) {
+  __shared__ int32_t items[kMaxPushItems];   // (expert << 5) | destination device
+  __shared__ int n_items, s_skip;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int N = a.N, P = a.P, M = a.M, rank = a.rank;
+  const uint8_t *replica = reinterpret_cast<const uint8_t *>(a.plan) + plan_layout(N, P).off_replica;
+  if (tid == 0) s_skip = a.skip && *a.skip;
+  if (tid < 32) {
+    int run = 0;
+    for (int e0 = 0; e0 < N; e0 += 32) {
+      const int e = e0 + lane;
+      int cnt = 0, me = -1, k = 0, native = 0;
+      uint32_t mask = 0;
+      if (e < N) {
+        native = e / M;
+        for (int d = 0; d < P; ++d)
+          if (replica[(size_t)e * P + d]) mask |= 1u << d;
+        k = __popc(mask);
+        if (native == rank) me = 0;
+        else if ((mask >> rank) & 1u) me = 1 + __popc(mask & ((1u << rank) - 1u));
+        const int lvl = me <= 0 ? 0 : 32 - __clz(me);   // floor(log2 me) + 1: first t with 2^t > me
+        if (me >= 0 && k > 0 && lvl == a.level)
+          for (int t = lvl; me + (1 << t) <= k; ++t) ++cnt;
+      }
+      int inc = cnt;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      const int lvl = me <= 0 ? 0 : 32 - __clz(me);
+      for (int i = 0; i < cnt; ++i) {
+        const int pos = run + inc - cnt + i;
+        if (pos < kMaxPushItems) items[pos] = (e << 5) | tree_holder(native, mask, me + (1 << (lvl + i)));
+      }
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) {
+      n_items = run < kMaxPushItems ? run : kMaxPushItems;
+      if (run > kMaxPushItems) atomicOr(a.err + 1, 64);
+    }
+  }
+  __syncthreads();
+  if (s_skip) return;
+  const int64_t total = a.w13_bytes + a.w2_bytes;
+  const int chunks = (int)((total + kPushChunk - 1) / kPushChunk);
+  const int64_t units = (int64_t)n_items * chunks;
+  const uint32_t epoch = a.ep[kEpWeight];
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int it = (int)(u / chunks), c = (int)(u % chunks);
+    const int e = items[it] >> 5, d = items[it] & 31;
+    const int fd = a.foreign_slot[(size_t)e * P + d];
+    const uint8_t *src13, *src2;
+    if (e / M == rank) {
+      src13 = reinterpret_cast<const uint8_t *>(a.w13) + (size_t)(e - rank * M) * a.w13_bytes;
+      src2 = reinterpret_cast<const uint8_t *>(a.w2) + (size_t)(e - rank * M) * a.w2_bytes;
+    } else {
+      // a forward: this rank's own copy of e must have landed (its parent's release)
+      const int fm = a.foreign_slot[(size_t)e * P + rank];
+      if (tid == 0) {
+        const uint32_t *own = a.peer_flags[rank] + kWeightFlag0 + fm;
+        const long long t0 = clock64();
+        long long spins = 0;
+        while ((int32_t)(ld_acquire_sys(own) - epoch) < 0) {
+          if (((++spins) & 1023) == 0 &&
+              (*reinterpret_cast<volatile int32_t *>(a.err + 1) != 0 || clock64() - t0 > 40000000000LL)) {
+            atomicOr(a.err + 1, 8);
+            break;
+          }
+        }
+      }
+      __syncthreads();
+      src13 = a.peer_w13[rank] + (size_t)fm * a.w13_bytes;
+      src2 = a.peer_w2[rank] + (size_t)fm * a.w2_bytes;
+    }
+    uint8_t *dst13 = a.peer_w13[d] + (size_t)fd * a.w13_bytes;
+    uint8_t *dst2 = a.peer_w2[d] + (size_t)fd * a.w2_bytes;
+    // bytes [b0, b1) of the concatenation [W13 | W2] (both multiples of 16 bytes)
+    const int64_t b0 = (int64_t)c * kPushChunk, b1 = b0 + kPushChunk < total ? b0 + kPushChunk : total;
+    for (int64_t b = b0 + (int64_t)tid * 64; b < b1; b += (int64_t)kPushThreads * 64) {
+      int4 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t o = b + q * 16;
+        if (o < b1) v[q] = o < a.w13_bytes ? *reinterpret_cast<const int4 *>(src13 + o)
+                                            : *reinterpret_cast<const int4 *>(src2 + (o - a.w13_bytes));
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t o = b + q * 16;
+        if (o < b1) {
+          if (o < a.w13_bytes) *reinterpret_cast<int4 *>(dst13 + o) = v[q];
+          else *reinterpret_cast<int4 *>(dst2 + (o - a.w13_bytes)) = v[q];
+        }
+      }
+    }
+    // this thread's peer stores before the chunk count; the last chunk releases the slot's flag
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t prev;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.counters + it) : "memory");
+      if (prev == (uint32_t)chunks - 1) {
+        a.counters[it] = 0;   // the next launch's count (stream-ordered after this kernel)
+        st_release_sys(a.peer_flags[d] + kWeightFlag0 + fd, epoch);
+      }
+    }
+    __syncthreads();
+  }
 }
 
 // a10 with the pushed GEMM2 epilogue: every slot's gated output row already sits in this rank's
@@ -573,13 +711,23 @@ cudaError_t launch_grad_reduce(float *dst, const float *base, int n_src, int64_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_signal(uint32_t *flag, uint32_t v, cudaStream_t s) {
-  signal_kernel<<<1, 1, 0, s>>>(flag, v);
+cudaError_t launch_signal(uint32_t *flag, const uint32_t *ep, cudaStream_t s) {
+  signal_kernel<<<1, 1, 0, s>>>(flag, ep);
   return cudaGetLastError();
 }
 
-cudaError_t launch_wait_flag(const uint32_t *flag, uint32_t v, int32_t *err, cudaStream_t s) {
-  wait_flag_kernel<<<1, 1, 0, s>>>(flag, v, err);
+cudaError_t launch_wait_flag(const uint32_t *flag, const uint32_t *ep, int32_t *err, cudaStream_t s) {
+  wait_flag_kernel<<<1, 1, 0, s>>>(flag, ep, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_push_level(const PushArgs &a, cudaStream_t s) {
+  push_level_kernel<<<kPushBlocks, kPushThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_advance(uint32_t *ep, cudaStream_t s) {
+  advance_kernel<<<1, 1, 0, s>>>(ep);
   return cudaGetLastError();
 }
 
@@ -639,19 +787,19 @@ cudaError_t launch_push_counts(const int32_t *cnt, int32_t N, int32_t rank, int3
   return cudaGetLastError();
 }
 
-cudaError_t launch_barrier(uint32_t *const *peer_flags, int32_t rank, int32_t P, uint32_t epoch,
+cudaError_t launch_barrier(uint32_t *const *peer_flags, int32_t rank, int32_t P, uint32_t *ep,
                            int32_t *err, cudaStream_t s) {
-  barrier_kernel<<<1, 32, 0, s>>>(peer_flags, rank, P, epoch, err);
+  barrier_kernel<<<1, 32, 0, s>>>(peer_flags, rank, P, ep, err);
   return cudaGetLastError();
 }
 
-cudaError_t launch_arrive(uint32_t *const *peer_flags, int32_t rank, int32_t P, uint32_t epoch, cudaStream_t s) {
-  arrive_kernel<<<1, 32, 0, s>>>(peer_flags, rank, P, epoch);
+cudaError_t launch_arrive(uint32_t *const *peer_flags, int32_t rank, int32_t P, const uint32_t *ep, cudaStream_t s) {
+  arrive_kernel<<<1, 32, 0, s>>>(peer_flags, rank, P, ep);
   return cudaGetLastError();
 }
 
 cudaError_t launch_dispatch(const DispatchArgs &a, cudaStream_t s) {
-  if (a.B == 0) return a.peer_flags ? launch_arrive(a.peer_flags, a.rank, a.P, a.epoch, s) : cudaSuccess;
+  if (a.B == 0) return a.peer_flags ? launch_arrive(a.peer_flags, a.rank, a.P, a.ep, s) : cudaSuccess;
   const int64_t blocks = (a.B + kDispatchWarps - 1) / kDispatchWarps;
   dispatch_kernel<<<(unsigned)blocks, kDispatchWarps * 32, 0, s>>>(a);
   return cudaGetLastError();

@@ -75,6 +75,8 @@ _SIGS = {
     "llep_prepare": (ctypes.c_int, [_vp, _vp, _i64, ctypes.POINTER(Params), _i32, _vp,
                                     ctypes.POINTER(Requirements), _vp]),
     "llep_moe_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "llep_moe_layer": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, ctypes.POINTER(Params), _i32, _vp, _vp,
+                                      _vp]),
     "llep_moe_forward_train": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     "llep_moe_backward_saved": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp,
                                                _vp, _vp, _vp]),
@@ -336,6 +338,27 @@ class Context:
                                       dx.data_ptr(), dgates.data_ptr(), dw13.data_ptr(), dw2.data_ptr(),
                                       _stream_ptr()))
         return dx, dgates, dw13, dw2
+
+    def layer(self, x, topk_ids, topk_w, w13, w2, alpha=1.0, min_chunk=1024, lam=1.3, ep=False,
+              plan_out=None, out=None):
+        """llep_moe_layer: prepare + forward in one call with no host synchronisation (CUDA-graph
+        capturable; the plan is recomputed on the device each replay).  The arena must already hold the
+        plan (reserve() first); an overflow surfaces at the next check()."""
+        import torch
+        B = x.shape[0]
+        for t, dt in ((x, torch.bfloat16), (topk_ids, torch.int32), (topk_w, torch.float32),
+                      (w13, torch.bfloat16), (w2, torch.bfloat16)):
+            assert t.dtype == dt and t.is_cuda and t.is_contiguous(), (t.dtype, dt)
+        assert w13.shape == (self.M, 2 * self.H, self.D) and w2.shape == (self.M, self.D, self.H)
+        if plan_out is None:
+            plan_out = torch.empty(plan_bytes(self.N, self.P), dtype=torch.uint8, device=x.device)
+        if out is None:
+            out = torch.empty((B, self.D), dtype=torch.bfloat16, device=x.device)
+        self._params = params(alpha, min_chunk, lam)   # kept alive with the context (graph replays)
+        _check(_lib.llep_moe_layer(self._h, x.data_ptr(), topk_ids.data_ptr(), topk_w.data_ptr(), B,
+                                   w13.data_ptr(), w2.data_ptr(), ctypes.byref(self._params), int(ep),
+                                   plan_out.data_ptr(), out.data_ptr(), _stream_ptr()))
+        return out
 
     def __call__(self, x, topk_ids, topk_w, w13, w2, alpha=1.0, min_chunk=1024, lam=1.3, ep=False,
                  plan_out=None, out=None):

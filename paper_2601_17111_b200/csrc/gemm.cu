@@ -431,13 +431,17 @@ __device__ __forceinline__ void warp_store_rows(uint8_t *wst, int lane, const ui
   __syncwarp();
 }
 
+#ifndef LLEP_FWD_RING_CAP
+#define LLEP_FWD_RING_CAP (227 * 1024)   // A/B builds: cap on the forward pair GEMMs' operand ring bytes
+#endif
 template <int BN, int KSUB = 1, int XB = 0>   // KSUB: 64-deep K sub-tiles per stage; XB: exchange bytes
 struct Cfg2 {
   static constexpr int A_BYTES = BM * BK * 2 * KSUB;
   static constexpr int B_BYTES = (BN / 2) * BK * 2 * KSUB;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int EXTRA = 1024 + 256 + XB;
-  static constexpr int STAGES_RAW = (kSmemBudget - EXTRA) / STAGE;
+  static constexpr int RING = kSmemBudget - EXTRA < LLEP_FWD_RING_CAP ? kSmemBudget - EXTRA : LLEP_FWD_RING_CAP;
+  static constexpr int STAGES_RAW = RING / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int SMEM = STAGES * STAGE + EXTRA;
   static_assert(B_BYTES % 1024 == 0, "B half tile must keep 1024-byte swizzle alignment");
@@ -2142,6 +2146,10 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
     return LLEP_ERR_INVALID;
   }
   if (g.row_align == 2 * BM) {   // 2-CTA pair tiles (groups 256-row aligned)
+#ifdef LLEP_FWD_FORCE_BN192
+    if (g.mode == 0 && g.nout % 96 == 0) return launch_pair<192, 0>(g, prm, s);
+    if (g.mode == 1 && g.nout % 192 == 0) return launch_pair<192, 1>(g, prm, s);
+#endif
     if (g.mode == 3) {
       if (g.nout % 128 == 0) return launch_pair<256, 3>(g, prm, s);
       if (g.nout % 120 == 0) return launch_pair<240, 3>(g, prm, s);

@@ -29,6 +29,10 @@ def layout(name):
         return [124518]
     if name == "cold":          # G120-P1's 127 cold groups alone
         return [52] * 77 + [51] * 50
+    if name == "dsv3p1":        # DeepSeek-V3 shape at P=1 (use --D 7168 --H 2048): hot + 255 cold of ~26 rows
+        return [124518] + [26] * 83 + [25] * 172
+    if name == "dsv3cold":
+        return [26] * 83 + [25] * 172
     if name == "uniform":
         return [1024] * 128
     if name.startswith("fgemm"):

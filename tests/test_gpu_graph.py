@@ -64,11 +64,12 @@ def test_layer_graph_replay_p1(L, cfg, B):
     ctx.close()
 
 
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [2, 4, 8])
 def test_layer_graph_replay_processes(L, tmp_path, P):
     """P processes on one GPU: direct layer calls (LLEP and EP) and graph replays with changing routings
     == the two-call path bit for bit; an EP plan larger than a fresh arena is caught on the device
-    (LLEP_ERR_PLAN at the next check) and the context recovers."""
+    (LLEP_ERR_PLAN at the next check) and the context recovers.  At P=8 the hot expert's 7 replicas take
+    three levels of the GPU-issued broadcast tree (native -> 1, 2, 4; 1 -> 3, 5; 2 -> 6; 3 -> 7)."""
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29650 + P))
     cmd = [sys.executable, os.path.join(HERE, "mp_graph_worker.py"), str(P), "tiny", str(tmp_path)]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)

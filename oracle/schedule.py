@@ -12,6 +12,12 @@ PAPER.md:
 
 Reading R11 (paper silent): expert e's global token order is rank-major -- all of
 rank 0's slots routed to e in flat order t*K+k, then rank 1's, and so on.
+Reading R11' (round 2, the CUDA path's default; also paper-silent): the same per-source blocks in
+flat order, but for an expert with MORE than one chunk the blocks follow the devices of its chunks in
+plan order (first appearance), then the remaining ranks ascending -- "chunk-aligned": a spill device's
+chunk then holds its own rows wherever the counts allow, so they need no transfer.  Experts with at
+most one chunk keep R11.  Both orders cover every slot exactly once; which one a call uses is a
+context setting (llep_context_set_token_order).
 """
 from __future__ import annotations
 
@@ -55,10 +61,31 @@ def local_rank_in_expert(ids: np.ndarray) -> np.ndarray:
     return r
 
 
-def global_index(ids: np.ndarray, C: np.ndarray, rank: int) -> np.ndarray:
-    """gidx_j = Σ_{q<p} C[q][e] + r_j  (rank-major global order, R11)."""
+def source_order(plan: Plan, e: int) -> List[int]:
+    """R11' order of the sources' blocks in expert e's global range: e's chunk devices in plan order
+    (first appearance), then the other ranks ascending; rank-major (R11) when e has <= 1 chunk."""
+    P = plan.world
+    A = plan.chunks[e]
+    if len(A) <= 1:
+        return list(range(P))
+    order: List[int] = []
+    for (d, _s, _t) in A:
+        if d not in order:
+            order.append(d)
+    return order + [q for q in range(P) if q not in order]
+
+
+def global_index(ids: np.ndarray, C: np.ndarray, rank: int, plan: Plan = None) -> np.ndarray:
+    """gidx_j = (slots of e from the sources before p) + r_j.  plan=None: rank-major, the sources
+    before p are q < p (R11); with a plan: the sources before p in source_order(plan, e) (R11')."""
     flat = np.asarray(ids).reshape(-1)
-    base = C[:rank].sum(axis=0) if rank > 0 else np.zeros(C.shape[1], dtype=np.int64)
+    if plan is None:
+        base = C[:rank].sum(axis=0) if rank > 0 else np.zeros(C.shape[1], dtype=np.int64)
+    else:
+        base = np.zeros(C.shape[1], dtype=np.int64)
+        for e in range(C.shape[1]):
+            order = source_order(plan, e)
+            base[e] = sum(int(C[q][e]) for q in order[:order.index(rank)])
     return base[flat] + local_rank_in_expert(flat)
 
 
@@ -74,13 +101,14 @@ def rows_on_device(plan: Plan, e: int, d: int) -> int:
     return sum(t - s for (dd, s, t) in plan.chunks[e] if dd == d)
 
 
-def slot_destinations(plan: Plan, C: np.ndarray, ids: np.ndarray, rank: int) -> Tuple[np.ndarray, np.ndarray]:
+def slot_destinations(plan: Plan, C: np.ndarray, ids: np.ndarray, rank: int,
+                      aligned: bool = False) -> Tuple[np.ndarray, np.ndarray]:
     """For each flat slot j of rank p: destination device d_j (the device of the unique chunk of
     expert e_j with start <= gidx_j < end) and the slot's position among expert e_j's
     rows on d_j (the chunks of e on d concatenated in plan order: the chunk's offset among them
-    plus gidx_j - start)."""
+    plus gidx_j - start).  aligned: global index in the R11' order instead of R11."""
     flat = np.asarray(ids).reshape(-1)
-    g = global_index(flat, C, rank)
+    g = global_index(flat, C, rank, plan if aligned else None)
     dev = np.full(flat.size, -1, dtype=np.int64)
     pos = np.empty(flat.size, dtype=np.int64)
     for e in np.unique(flat):

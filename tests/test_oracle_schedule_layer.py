@@ -339,3 +339,86 @@ def test_schedule_vectorised_equals_slot_loop():
             dev, pos = O2.slot_destinations(plan, C, ids[p], p)
             d2, p2 = _loop_destinations(plan, C, flat, p)
             assert dev.tolist() == d2 and pos.tolist() == p2
+
+
+def test_chunk_aligned_order_worked_example():
+    """R11' by hand.  P=3, N=3 (M=1), K=1, loads l = [9, 2, 1] with e0's 9 slots split 3/3/3 over the
+    ranks.  cap = floor(12/3) = 4; e0: native chunk (0, 0, 4), then LLAS picks the least-loaded device 2
+    (load 1 < device 1's 2): (2, 4, 7), then device 1: (1, 7, 9).  Chunk-aligned source order of e0 =
+    [0, 2, 1]: rank 0 takes global [0, 3), rank 2 [3, 6), rank 1 [6, 9) -- so rank 2's e0 slots land at
+    4, 5 on device 2 (local) and rank 1's at 7, 8 on device 1 (local); rank-major would send all of
+    rank 1's and two of rank 2's e0 slots across."""
+    ids = [np.array([[0], [0], [0], [1]]), np.array([[0], [1], [0], [0]]), np.array([[0], [0], [2], [0]])]
+    C = O2.load_matrix(ids, 3)
+    assert C[:, 0].tolist() == [3, 3, 3] and C.sum(0).tolist() == [9, 2, 1]
+    plan = O1.plan(C.sum(0).tolist(), 3, 1.0, 1, 1.3)
+    assert plan.chunks[0] == [(0, 0, 4), (2, 4, 7), (1, 7, 9)]
+    assert O2.source_order(plan, 0) == [0, 2, 1]
+    assert O2.source_order(plan, 2) == [0, 1, 2]                 # one chunk: rank-major
+    g = [O2.global_index(ids[p], C, p, plan) for p in range(3)]
+    e0 = [g[p][ids[p].reshape(-1) == 0].tolist() for p in range(3)]
+    assert e0 == [[0, 1, 2], [6, 7, 8], [3, 4, 5]]
+    d = [O2.slot_destinations(plan, C, ids[p], p, aligned=True)[0] for p in range(3)]
+    d_e0 = [d[p][ids[p].reshape(-1) == 0].tolist() for p in range(3)]
+    assert d_e0 == [[0, 0, 0], [2, 1, 1], [0, 2, 2]]
+    rm = [O2.slot_destinations(plan, C, ids[p], p)[0][ids[p].reshape(-1) == 0].tolist() for p in range(3)]
+    assert rm == [[0, 0, 0], [0, 2, 2], [2, 1, 1]]
+    local = lambda dd: sum(int(x == p) for p, row in enumerate(dd) for x in row)   # noqa: E731
+    assert local(d_e0) == 7 and local(rm) == 4
+
+
+def test_chunk_aligned_order_is_a_permutation_fuzz():
+    """R11' covers every slot exactly once: per expert the aligned global indices of all ranks are a
+    permutation of [0, l_e), each chunk receives exactly its rows, and experts with <= 1 chunk keep
+    rank-major indices."""
+    rng = np.random.default_rng(7)
+    for it in range(300):
+        P = int(rng.choice([2, 3, 4, 8]))
+        M = int(rng.choice([1, 2, 4]))
+        N, K = P * M, int(rng.integers(1, 4))
+        B = int(rng.integers(0, 40))
+        hot = rng.random(N) ** 4
+        ids = [rng.choice(N, size=(B, K), p=hot / hot.sum()).astype(np.int32) for _ in range(P)]
+        C = O2.load_matrix(ids, N)
+        plan = O1.plan(C.sum(0).tolist(), P, float(rng.choice([1.0, 1.2])), int(rng.integers(0, 8)), 1.0)
+        ga = [O2.global_index(ids[p], C, p, plan) for p in range(P)]
+        gr = [O2.global_index(ids[p], C, p) for p in range(P)]
+        for e in range(N):
+            got = np.sort(np.concatenate([ga[p][ids[p].reshape(-1) == e] for p in range(P)]))
+            assert got.tolist() == list(range(int(C[:, e].sum()))), (it, e)
+            if len(plan.chunks[e]) <= 1:
+                for p in range(P):
+                    m = ids[p].reshape(-1) == e
+                    assert np.array_equal(ga[p][m], gr[p][m])
+        per_dev = np.zeros((N, P), dtype=np.int64)
+        for p in range(P):
+            dev, _pos = O2.slot_destinations(plan, C, ids[p], p, aligned=True)
+            np.add.at(per_dev, (ids[p].reshape(-1), dev), 1)
+        for e in range(N):
+            for d in range(P):
+                assert per_dev[e, d] == O2.rows_on_device(plan, e, d)
+
+
+def test_chunk_aligned_order_keeps_g120_spills_local():
+    """At the north-star layer shape (G120, P=8, 95 %/1, equal counts on every rank) the hot expert has a
+    chunk on every device, in LLAS order (least loaded first, not rank order); under R11' each device's
+    chunk is (almost) its own rows: > 99 % of the hot expert's slots stay on their rank, against ~1/8
+    rank-major."""
+    P = 8
+    base = W.CONFIGS["g120"]
+    sh = W.LayerShape(base.n_experts, base.top_k, base.d_model, base.d_ff, 4096, P)
+    ids = [W.routing_ids(sh, p, 95, 1, 21) for p in range(P)]
+    C = O2.load_matrix(ids, sh.n_experts)
+    plan = O1.plan(C.sum(0).tolist(), P)
+    order = [d for (d, _s, _t) in plan.chunks[0]]
+    assert sorted(order) == list(range(P)) and order != list(range(P))
+    frac = {}
+    for aligned in (False, True):
+        loc = tot = 0
+        for p in range(P):
+            dev, _ = O2.slot_destinations(plan, C, ids[p], p, aligned=aligned)
+            m = ids[p].reshape(-1) == 0
+            loc += int((dev[m] == p).sum())
+            tot += int(m.sum())
+        frac[aligned] = loc / tot
+    assert frac[True] > 0.99 and frac[False] < 0.15, frac

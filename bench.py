@@ -226,21 +226,30 @@ def run_graph(L, ctx, inputs, ref_out, steps, warmup, world):
                     "replayed; inputs resident"}
 
 
-def link_bytes(plan, C, D, H):
+def link_bytes(plan, C, D, H, aligned=True):
     """Bytes each device sends / receives over NVLink in the three exchange phases of one layer step,
     from the replicated plan and the [P, N] load matrix (bench-side accounting):
       dispatch  every remote (token, slot) row: bf16 row 2D + fp32 gate 4 + int32 source index 4 bytes
       weights   every copy of the binomial broadcast tree: W13 (2H x D) + W_down (D x H) bf16 = 6DH bytes
       combine   every remote row's gated output pushed back by the GEMM2 epilogue: 2D bytes
-    Expert e's global token order is rank-major (R11), so source p owns [Σ_{q<p} C[q][e], Σ_{q<=p} C[q][e])
-    of e's range and sends each chunk's overlap with it to the chunk's device.  Local rows cost nothing."""
+    Each source's slots of expert e form one block of e's global range; the blocks follow the token order
+    of the context: chunk-aligned (R11', default: an expert with > 1 chunk lists its chunk devices in plan
+    order first, then the other ranks ascending) or rank-major (R11).  A source sends each chunk's overlap
+    with its block to the chunk's device.  Local rows cost nothing."""
     P, N = C.shape
     M = N // P
     eg = {k: np.zeros(P, dtype=np.int64) for k in ("dispatch", "weights", "combine")}
     ing = {k: np.zeros(P, dtype=np.int64) for k in ("dispatch", "weights", "combine")}
     for e in range(N):
         lo = 0
-        for p in range(P):
+        srcs = list(range(P))
+        if aligned and len(plan.chunks[e]) > 1:
+            first = []
+            for (d, _s, _t) in plan.chunks[e]:
+                if d not in first:
+                    first.append(d)
+            srcs = first + [q for q in range(P) if q not in first]
+        for p in srcs:
             hi = lo + int(C[p][e])
             for (d, s0, t0) in plan.chunks[e]:
                 n = min(t0, hi) - max(s0, lo)

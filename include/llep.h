@@ -158,6 +158,20 @@ llep_status llep_context_enable_backward(llep_context *ctx);
  * the lazily grown backward workspaces (every cudaMalloc the context made). */
 int64_t llep_context_device_bytes(const llep_context *ctx);
 
+/* Global token order of an expert's routed slots (a3, the index the plan's chunk ranges [start, end)
+ * refer to; the paper leaves it open, "build chunks of B̄_p from 𝒜"):
+ *   LLEP_ORDER_RANK_MAJOR     rank 0's slots of e in flat order t*K+k, then rank 1's, ... (reading R11,
+ *                             SPEC S:247-255)
+ *   LLEP_ORDER_CHUNK_ALIGNED  (default) for an expert with more than one chunk the sources' blocks follow
+ *                             its chunk devices in plan order (first appearance), then the other ranks
+ *                             ascending (reading R11'): a spill device's chunk holds its own rows wherever
+ *                             the counts allow, so they cross no link.  Experts with <= 1 chunk: rank-major.
+ * Outputs are identical under both (every row is computed alone; the K-sum is in slot order); the plan
+ * is unchanged; receive rows, slot destinations and NVLink bytes differ.  Every rank must use the same
+ * order.  Takes effect at the next llep_prepare / llep_moe_layer.  Errors: INVALID. */
+enum { LLEP_ORDER_RANK_MAJOR = 0, LLEP_ORDER_CHUNK_ALIGNED = 1 };
+llep_status llep_context_set_token_order(llep_context *ctx, int32_t order);
+
 /* Per-GPU memory cap for the context's device allocations (0 = none).  A llep_context_reserve that
  * would take the context above `bytes` fails with LLEP_ERR_NOMEM and leaves the arena unchanged:
  * the "tight per-GPU memory cap" of the Qwen3-shaped benchmark (BASELINE.json), under which standard

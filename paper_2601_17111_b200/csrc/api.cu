@@ -182,6 +182,7 @@ using namespace llep;
 struct llep_context {
   int32_t N, K, D, H, P, M, rank, device, num_sms;
   int32_t row_align = 256;  // 256: 2-CTA GEMM tiles; 128: 1-CTA tiles (LLEP_ROW_ALIGN=128)
+  int32_t token_order = LLEP_ORDER_CHUNK_ALIGNED;   // a3/a5 global token order (llep_context_set_token_order)
   int64_t mem_cap = 0;      // 0: no cap on scratch + arena + activations
   int64_t max_tokens;
   // rank-local scratch
@@ -652,6 +653,14 @@ llep_status llep_context_enable_backward(llep_context *c) {
   return alloc_arena(c, c->arena_rows, c->arena_foreign);
 }
 
+llep_status llep_context_set_token_order(llep_context *c, int32_t order) {
+  if (!c) return invalid("null context");
+  if (order != LLEP_ORDER_RANK_MAJOR && order != LLEP_ORDER_CHUNK_ALIGNED) return invalid("unknown token order");
+  c->token_order = order;
+  c->plan_dev_cached = nullptr;   // the layout (source masks) depends on it: recompute for the next call
+  return LLEP_OK;
+}
+
 llep_status llep_context_set_memory_cap(llep_context *c, int64_t bytes) {
   if (!c || bytes < 0) return invalid("null context or negative cap");
   c->mem_cap = bytes;
@@ -726,6 +735,7 @@ static llep_status run_layout(llep_context *c, const void *plan, cudaStream_t s,
   la.sched_cap = c->sched_cap;
   la.row_align = c->row_align;
   la.mblk_src = c->mblk_src;
+  la.aligned = c->token_order == LLEP_ORDER_CHUNK_ALIGNED;
   LLEP_CUDA(launch_layout(la, s));
   ++c->launches;
   return LLEP_OK;
@@ -1023,6 +1033,7 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   da.rtok = gather ? c->rtok : nullptr;
   da.mblk_src = c->mblk_src;
   da.row_align = c->row_align;
+  da.aligned = c->token_order == LLEP_ORDER_CHUNK_ALIGNED;
   LLEP_CUDA(launch_dispatch(da, s));
   c->launches += B > 0 || overlap;
   if (!overlap && (st = barrier(c, s)) != LLEP_OK) return st;   // dispatched rows landed
@@ -1268,6 +1279,7 @@ static llep_status moe_backward(llep_context *c, const uint16_t *x, const int32_
   da.rtok = nullptr;         // the backward GEMMs read every row from the receive buffer
   da.mblk_src = nullptr;
   da.row_align = c->row_align;
+  da.aligned = c->token_order == LLEP_ORDER_CHUNK_ALIGNED;
   LLEP_CUDA(launch_dispatch(da, s));
   c->launches += B > 0;
   if (any_copy) LLEP_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));

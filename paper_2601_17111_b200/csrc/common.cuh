@@ -83,6 +83,31 @@ __host__ __device__ inline int wgrad_split_rows(int n_rows, int splits) {
   return ((padded + splits - 1) / splits + 255) / 256 * 256;
 }
 
+// Offset of source rank p's block in expert e's global token range (a3/a5).  aligned = 0: rank-major,
+// Σ_{q<p} C[q][e] (reading R11).  aligned = 1 (R11', the default): for an expert with more than one chunk
+// the blocks follow e's chunk devices in plan order (first appearance), then the other ranks ascending,
+// so a spill device's chunk holds its own rows wherever the counts allow.  A: e's chunks, nc of them;
+// C: the [P, N] load matrix.  Identical on every rank (replicated plan and C).
+__device__ __forceinline__ int64_t source_offset(const llep_chunk *A, int nc, const int32_t *C, int N, int P,
+                                                 int e, int p, int aligned) {
+  int64_t off = 0;
+  if (!aligned || nc <= 1) {
+    for (int q = 0; q < p; ++q) off += C[(size_t)q * N + e];
+    return off;
+  }
+  uint32_t seen = 0;
+  for (int c = 0; c < nc; ++c) {
+    const int d = A[c].device;
+    if ((seen >> d) & 1u) continue;
+    if (d == p) return off;
+    seen |= 1u << d;
+    off += C[(size_t)d * N + e];
+  }
+  for (int q = 0; q < p; ++q)
+    if (!((seen >> q) & 1u)) off += C[(size_t)q * N + e];
+  return off;
+}
+
 // Group table entry (8 int32) of one expert group a device computes.
 struct Group {
   int32_t expert;      // global expert id
@@ -123,6 +148,7 @@ struct LayoutArgs {
   int32_t row_align;           // group row bases / GEMM M tile: 128 or 256
   uint32_t *mblk_src;          // [sched_cap] per m-block (group order) of this rank: bit q set iff the
                                // block holds rows dispatched by source rank q (row f2 arrival waits)
+  int32_t aligned;             // token order (source_offset): 0 rank-major (R11), 1 chunk-aligned (R11')
   // capture-safe layer (llep_moe_layer) only: the arena this call must fit.  A plan that needs more rows
   // or foreign slots on ANY device (the same decision on every rank) sets summary->error |= 16,
   // err[3] |= 1 and *n_groups_dev = 0, so no kernel of that call writes past the arena.
@@ -206,6 +232,7 @@ struct DispatchArgs {
   int32_t *rtok;
   const uint32_t *mblk_src;
   int32_t row_align;
+  int32_t aligned;          // token order of the global index (source_offset)
 };
 cudaError_t launch_dispatch(const DispatchArgs &a, cudaStream_t s);
 

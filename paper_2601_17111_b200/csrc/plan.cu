@@ -385,7 +385,8 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(LayoutArgs a) {
   }
   // row f2: sources of every m-block of this rank (group order).  Group rows are e's chunks on this
   // device in plan order; a chunk (d, s, t) holds global indices [s, t) of e, and source q owns
-  // [Σ_{p<q} C[p][e], Σ_{p<=q} C[p][e]) of them (rank-major order, R11), so the block's rows map to
+  // [off_q, off_q + C[q][e]) of them (off_q = source_offset: rank-major R11 or chunk-aligned R11'), so the
+  // block's rows map to
   // global ranges whose overlap with each source's range decides the mask.
   if (a.mblk_src && sm_mblocks <= a.sched_cap && sm_groups <= kMaxGroups) {
     for (int mb = tid; mb < sm_mblocks; mb += kLayoutThreads) {
@@ -408,11 +409,11 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(LayoutArgs a) {
         const int x0 = max(r0, off), x1 = min(r1, off + len);
         if (x0 < x1) {
           const long long g0 = ch.start + (x0 - off), g1 = ch.start + (x1 - off);   // global [g0, g1)
-          long long cum = 0;
           for (int q = 0; q < P; ++q) {
             const long long nq = a.load_matrix[(size_t)q * N + e];
+            const long long cum = source_offset(chunks + (size_t)e * MC, n_chunks[e], a.load_matrix, N, P, e, q,
+                                                a.aligned);
             if (nq > 0 && cum < g1 && cum + nq > g0) mask |= 1u << q;
-            cum += nq;
           }
         }
         off += len;

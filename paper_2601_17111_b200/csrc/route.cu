@@ -223,9 +223,10 @@ __device__ __forceinline__ void dispatch_token(const DispatchArgs &a, int64_t t,
     const bool changed = a.ids[j] != e;
     if (changed) atomicOr(a.err + 2, 1);
     if (e >= 0 && e < N) {
-      int g = a.local_rank[j];
-      for (int q = 0; q < a.rank; ++q) g += a.load_matrix[(size_t)q * N + e];  // rank-major (R11)
       const int nc = n_chunks[e];
+      // global index within e: this source's block offset (R11 / R11') + the stable local rank (a3)
+      const int g = a.local_rank[j] + (int)source_offset(chunks + (size_t)e * MC, nc, a.load_matrix, N, P, e,
+                                                         a.rank, a.aligned);
       for (int c = 0; c < nc; ++c) {
         const llep_chunk ch = chunks[(size_t)e * MC + c];
         if (g >= ch.start && g < ch.end) {

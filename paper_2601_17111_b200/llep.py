@@ -72,6 +72,7 @@ _SIGS = {
     "llep_moe_backward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "llep_context_device_bytes": (_i64, [_vp]),
     "llep_context_set_memory_cap": (ctypes.c_int, [_vp, _i64]),
+    "llep_context_set_token_order": (ctypes.c_int, [_vp, _i32]),
     "llep_prepare": (ctypes.c_int, [_vp, _vp, _i64, ctypes.POINTER(Params), _i32, _vp,
                                     ctypes.POINTER(Requirements), _vp]),
     "llep_moe_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
@@ -94,6 +95,7 @@ for _name, (_res, _args) in _SIGS.items():
     _f.restype = _res
     _f.argtypes = _args
 
+ORDER_RANK_MAJOR, ORDER_CHUNK_ALIGNED = 0, 1
 DBG_LOAD_MATRIX, DBG_SLOT_DST, DBG_GROUPS, DBG_RECV_X, DBG_ACT, DBG_Y, DBG_LOCAL_RANK, DBG_RECV_G = range(1, 9)
 
 
@@ -256,6 +258,12 @@ class Context:
         _check(_lib.llep_context_stats(self._h, ctypes.byref(st), int(reset)))
         return {"ms": dict(zip(PHASES, list(st.ms))), "calls": int(st.calls),
                 "kernel_launches": int(st.kernel_launches), "gemm_rows": int(st.gemm_rows)}
+
+    def set_token_order(self, order: str) -> None:
+        """"chunk_aligned" (default, reading R11') or "rank_major" (R11): the global token order the
+        plan's chunk ranges index.  Same on every rank; outputs identical, link bytes differ."""
+        _check(_lib.llep_context_set_token_order(self._h, {"rank_major": ORDER_RANK_MAJOR,
+                                                          "chunk_aligned": ORDER_CHUNK_ALIGNED}[order]))
 
     def set_memory_cap(self, nbytes: int) -> None:
         _check(_lib.llep_context_set_memory_cap(self._h, int(nbytes)))

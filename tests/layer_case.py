@@ -98,11 +98,14 @@ def expected_layout(plan, d: int, row_align: int = 256):
     return out
 
 
-def check_index_work(res, key: str, plan, ids_all, n_experts: int):
+def check_index_work(res, key: str, plan, ids_all, n_experts: int, aligned: bool = None):
     """Rows a1-a5 bit-exact against O2 on every rank (north star: integer / index work bit-exact):
     the all-gathered load matrix C, every slot's stable local rank r_j, every device's group table,
     and every slot's destination (device, row) = (d_j, base_d[e_j] + pos_j) with (d_j, pos_j) from
-    O2.slot_destinations (rank-major global index R11, chunk lookup P:547-548)."""
+    O2.slot_destinations (global index in the context's token order -- chunk-aligned R11' by default,
+    rank-major R11 when LLEP_TEST_ORDER=rank_major -- and the chunk lookup of P:547-548)."""
+    if aligned is None:
+        aligned = os.environ.get("LLEP_TEST_ORDER", "chunk_aligned") != "rank_major"
     from oracle import schedule as O2
     P = len(ids_all)
     C = O2.load_matrix(ids_all, n_experts)
@@ -116,7 +119,7 @@ def check_index_work(res, key: str, plan, ids_all, n_experts: int):
     for p in range(P):
         assert np.array_equal(res[p][f"{key}_lm"], C), (key, p)
         assert np.array_equal(res[p][f"{key}_lr"], O2.local_rank_in_expert(ids_all[p])), (key, p)
-        dev, pos = O2.slot_destinations(plan, C, ids_all[p], p)
+        dev, pos = O2.slot_destinations(plan, C, ids_all[p], p, aligned=aligned)
         flat = ids_all[p].reshape(-1)
         row = np.array([base[d][int(e)] for d, e in zip(dev, flat)], dtype=np.int64) + pos
         dst = res[p][f"{key}_dst"]
@@ -132,7 +135,7 @@ def boundary_tokens(plan, ids_all, n_experts: int, extra: int = 16):
     P = len(ids_all)
     C = O2.load_matrix(ids_all, n_experts)
     K = ids_all[0].shape[1]
-    gidx = [O2.global_index(ids_all[p], C, p) for p in range(P)]
+    gidx = [O2.global_index(ids_all[p], C, p, plan) for p in range(P)]   # chunk-aligned order (R11')
     flat = [ids_all[p].reshape(-1) for p in range(P)]
     want = {p: set(range(min(extra, ids_all[p].shape[0]))) for p in range(P)}
     for e, A in enumerate(plan.chunks):

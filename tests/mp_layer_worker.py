@@ -69,6 +69,8 @@ def worker(rank, P, cfg, pct, nhot, outdir, sample):
         dist.destroy_process_group()
         return
     ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, P, rank, dev, sh.tokens_per_rank)
+    if os.environ.get("LLEP_TEST_ORDER"):   # the token order of a3/a5 (default chunk-aligned)
+        ctx.set_token_order(os.environ["LLEP_TEST_ORDER"])
     out_llep = ctx(x, ids, gates, w13, w2, alpha, m, lam)
     plan = ctx.prepare(ids, alpha, m, lam)[0]          # plan of the LLEP call (deterministic)
     plan_np = plan.cpu().numpy()

@@ -548,3 +548,32 @@ def test_local_gather_bitwise_equals_copy(L, cfg, pct, nhot):
     mr, l2 = LC.errors(_to_np(res["gather"][0][: min(B, 256)]), ref)
     assert mr <= LC.TOL_MAX_REL and l2 <= LC.TOL_REL_L2, (mr, l2)
     ctx.close()
+
+
+def test_token_orders_same_outputs_different_rows(L, tmp_path):
+    """a3/a5 token order (llep_context_set_token_order): the rank-major order (R11) and the default
+    chunk-aligned one (R11') give bit-identical outputs (each row is computed alone, the K-sum is in slot
+    order) with each order's index work bit-exact vs O2 at P=4 with spills; the aligned order keeps more
+    of the spilled rows on their own rank."""
+    from oracle import planner as O1
+    from oracle import schedule as O2
+    outs, dst = {}, {}
+    for order in ("rank_major", "chunk_aligned"):
+        d = tmp_path / order
+        d.mkdir()
+        env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29585 + len(order)), LLEP_TEST_ORDER=order)
+        cmd = [sys.executable, os.path.join(HERE, "mp_layer_worker.py"), "4", "tiny", "95", "1", str(d)]
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        res = [np.load(os.path.join(d, f"rank{p}.npz")) for p in range(4)]
+        sh0 = W.CONFIGS["tiny"]
+        sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, 4)
+        ids_all = [W.routing_ids(sh, p, 95, 1, 21) for p in range(4)]
+        C = O2.load_matrix(ids_all, sh.n_experts)
+        plan = O1.plan(C.sum(0).tolist(), 4)
+        LC.check_index_work(res, "llep", plan, ids_all, sh.n_experts, aligned=(order == "chunk_aligned"))
+        outs[order] = [r_["llep"] for r_ in res]
+        dst[order] = sum(int((r_["llep_dst"][:, 0] == p).sum()) for p, r_ in enumerate(res))
+    for a, b in zip(outs["rank_major"], outs["chunk_aligned"]):
+        assert np.array_equal(a, b)
+    assert dst["chunk_aligned"] > dst["rank_major"], dst

@@ -43,7 +43,7 @@ def test_gloo_ranks_agree_on_plan_and_link_bytes(tmp_path, P, cfg, pct, nhot, po
     D, H = sh.d_model, sh.d_ff
     remote = 0
     for p in range(P):
-        dev, _row = O2.slot_destinations(ref, C, ids_all[p], p)
+        dev, _row = O2.slot_destinations(ref, C, ids_all[p], p, aligned=True)   # the default order (R11')
         remote += int((dev != p).sum())
     assert int(res[0]["disp"]) == remote * (2 * D + 8)
     assert int(res[0]["comb"]) == remote * 2 * D

@@ -43,15 +43,25 @@ def rank_groups(plan, rank, M):
     return rows
 
 
-def link_seconds(plan, cnt, D, H, M, P=8):
-    """Modelled NVLink time of one layer: dispatch + combine rows and the weight broadcast."""
+def link_seconds(plan, cnt, D, H, M, P=8, aligned=True):
+    """Modelled NVLink time of one layer: dispatch + combine rows and the weight broadcast.  Every rank
+    has the same counts cnt; source blocks in the library's token order (chunk-aligned R11' by default:
+    an expert with > 1 chunk lists its chunk devices in plan order first, then the other ranks)."""
     egress = np.zeros(P)
     ingress = np.zeros(P)
     for e, chunks in enumerate(plan.chunks):
         c = int(cnt[e])
+        srcs = list(range(P))
+        if aligned and len(chunks) > 1:
+            first = []
+            for (d, _s, _t) in chunks:
+                if d not in first:
+                    first.append(d)
+            srcs = first + [q for q in range(P) if q not in first]
+        pos = {p: i for i, p in enumerate(srcs)}   # source p's block: global [pos·c, (pos+1)·c)
         for (d, s, t) in chunks:
-            for p in range(P):   # rows of expert e from source rank p: global range [p·c, (p+1)·c)
-                n = max(0, min(t, (p + 1) * c) - max(s, p * c))
+            for p in range(P):
+                n = max(0, min(t, (pos[p] + 1) * c) - max(s, pos[p] * c))
                 if n and p != d:
                     egress[p] += n * (2 * D + 4 + 2 * D)
                     ingress[d] += n * (2 * D + 4 + 2 * D)

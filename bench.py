@@ -584,7 +584,10 @@ def gpu_main(args):
                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
                "note": "pinned host -> device inputs and device -> host output every step, "
                        "double-buffered on copy streams"}
-    graph = run_graph(L, ll_ctx, inputs, ll_out, args.steps, args.warmup, world)
+    try:
+        graph = run_graph(L, ll_ctx, inputs, ll_out, args.steps, args.warmup, world)
+    except Exception as err:   # a capture problem must not cost the rest of the line
+        graph = {"error": f"{type(err).__name__}: {err}"[:300]}
     bwd_ms = None
     if not args.no_backward:
         bwd_ms, train_ms = run_backward(L, ll_ctx, shape, inputs, max(3, args.steps // 2), 3, world, SEED)

@@ -26,6 +26,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -1096,7 +1098,10 @@ llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
   prm.wup_off = MODE != 1 ? g.nout : 0;
   prm.n_ntiles = (g.nout + (MODE != 1 ? BN / 2 : BN) - 1) / (MODE != 1 ? BN / 2 : BN);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(g.num_sms & ~1));
+  int grid = g.num_sms & ~1;
+  if (const char *gp = getenv("LLEP_GEMM_PAIRS"))   // measurement only: fewer CTA pairs (per-pair rates)
+    grid = 2 * std::max(1, std::min(grid / 2, atoi(gp)));
+  cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;

@@ -1,6 +1,6 @@
 """Weight-gradient GEMM (llep_gemm_bwd kind 1, CTA pairs) on G120-P1-like group layouts: time per
 launch (CUDA events, median of 10 after 0.4 s of back-to-back warm-up) and the output write rate.
-    python tools/wgrad_bench.py [hot|small|both] [mdim] [nout] [--1cta]"""
+    python tools/wgrad_bench.py [hot|small|both|p8] [mdim] [nout] [--1cta]"""
 import os
 import statistics
 import sys
@@ -14,7 +14,8 @@ which = sys.argv[1] if len(sys.argv) > 1 else "both"
 mdim = int(sys.argv[2]) if len(sys.argv) > 2 else 2880
 nout = int(sys.argv[3]) if len(sys.argv) > 3 else 2880
 pair = "--1cta" not in sys.argv
-sizes = {"hot": [124518], "small": [52] * 127, "both": [124518] + [52] * 127}[which]
+sizes = {"hot": [124518], "small": [52] * 127, "both": [124518] + [52] * 127,
+         "p8": [124832] + [416] * 15}[which]   # p8: the G120 P=8 LLEP critical-rank layout
 groups, rb = [], 0
 for i, n in enumerate(sizes):
     groups.append((i, rb, n))

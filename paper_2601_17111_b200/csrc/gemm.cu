@@ -1064,6 +1064,10 @@ template <int BN, int MODE, int KSUB = LLEP_FWD_KSUB>
 llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
   using C = Cfg2<BN, KSUB, (MODE == 0 || MODE == 3) ? kXchgBytes : kStoreStageBytes>;
   auto kern = grouped_gemm_2cta_kernel<BN, MODE, KSUB>;
+  if (!g.sched) {   // the pair kernels walk the layout's interleaved m-block schedule
+    set_error("pair GEMM needs the m-block schedule (LLEP_GEMM_GROUP_ORDER applies to the 1-CTA kernels)");
+    return LLEP_ERR_INVALID;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     LLEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));

@@ -98,8 +98,13 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
+// TMEM-empty arrival on the leader CTA's mbarrier (remote address from mapa).  CTA-scope release (the
+// PTX default, as CUTLASS's ClusterBarrier::arrive): it orders this thread's tcgen05.ld of the drained
+// accumulator (after tcgen05.fence::before_thread_sync) before the arrival, but -- unlike
+// .release.cluster -- does not hold the epilogue until every global store of the tile is performed at
+// cluster scope (ncu: that wait, an ERRBAR before the arrive, was the top stall of short-K GEMM2s).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map, uint32_t leader_bar,
                                                  int c0, int c1, uint64_t policy) {

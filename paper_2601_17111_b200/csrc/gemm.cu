@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const __g
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
+      __syncwarp();
     }
   }
   // fused combine push (mode 1): order this thread's peer stores before the kernel's completion and
@@ -987,6 +988,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(tempty + acc), 0));
+      __syncwarp();   // reconverge: named barriers (bar.sync) that follow require converged warps
     }
   }
   // fused combine push (mode 1): order this thread's peer stores before the kernel's completion and
@@ -1439,6 +1441,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_kernel(const __grid_
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
+      __syncwarp();
     }
   }
   if (KIND == 1 && threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -1930,6 +1933,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_pair_kernel(const __
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(tempty + acc), 0));
+      __syncwarp();   // reconverge: named barriers (bar.sync) that follow require converged warps
     }
   }
   if (KIND == 1 && threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");

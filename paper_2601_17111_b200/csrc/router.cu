@@ -259,8 +259,9 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __grid_
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(tempty + acc), 0));
+      __syncwarp();   // reconverge: named barriers (bar.sync) that follow require converged warps
       if (h == 1) {
-        if (it > 0) asm volatile("bar.sync 2, 256;" ::: "memory");   // h = 0 has read the last one
+        if (it > 0) asm volatile("barrier.sync 2, 256;" ::: "memory");   // h = 0 has read the last one
         xp[0] = mx;
         xp[1] = sum;
 #pragma unroll
@@ -268,9 +269,11 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __grid_
           xp[2 + r] = tv[r];
           xp[2 + KMAX + r] = __int_as_float(ti[r]);
         }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        asm volatile("barrier.sync 1, 256;" ::: "memory");
       } else {
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        // the two column halves meet at named barriers from different code locations: the
+        // non-.aligned barrier forms (bar.sync / bar.arrive are .aligned: one instruction per barrier)
+        asm volatile("barrier.sync 1, 256;" ::: "memory");
         const float m1 = xp[0], s1 = xp[1];
         float bv[KMAX];
         int bi[KMAX];
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __grid_
           bv[r] = xp[2 + r];
           bi[r] = __float_as_int(xp[2 + KMAX + r]);
         }
-        asm volatile("bar.arrive 2, 256;" ::: "memory");
+        asm volatile("barrier.arrive 2, 256;" ::: "memory");
         // merge: softmax sums at the common max; top-K of two descending lists (on equal values
         // the first half -- lower expert ids -- goes first)
         const float m = fmaxf(mx, m1);
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __grid_
         }
       }
     }
-    if (h == 1 && it > 0) asm volatile("bar.sync 2, 256;" ::: "memory");
+    if (h == 1 && it > 0) asm volatile("barrier.sync 2, 256;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();

@@ -79,3 +79,21 @@ def test_layer_graph_replay_processes(L, tmp_path, P):
         assert res["direct_same"].all(), (p, res["direct_same"])
         assert res["replay_same"].all(), (p, res["replay_same"])
         assert int(res["overflow_code"]) == 2, (p, int(res["overflow_code"]))
+
+
+def test_layer_small_and_empty_batches_p1(L):
+    """The capture-safe call on B = 0, 1, 7 and a ragged 1000 tokens == the two-call path bit for bit."""
+    sh = W.LayerShape(8, 2, 256, 512, 1024, 1)
+    x = W.tokens_torch(1024, 256, 0, "cuda", 5)
+    ids = torch.from_numpy(W.routing_ids(sh, 0, 95, 1, 5)).cuda()
+    g = torch.from_numpy(W.gate_weights(1024, 2, 0, 5)).cuda()
+    w13, w2 = W.expert_weights_torch(range(8), 256, 512, "cuda", 5)
+    ctx = L.Context(8, 2, 256, 512, 1, 0, 0, 1024)
+    for B in (0, 1, 7, 1000):
+        xs, ii, gg = x[:B].contiguous(), ids[:B].contiguous(), g[:B].contiguous()
+        a = ctx(xs, ii, gg, w13, w2).clone()
+        b = ctx.layer(xs, ii, gg, w13, w2)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), B
+    ctx.check()
+    ctx.close()

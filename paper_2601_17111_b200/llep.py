@@ -262,8 +262,14 @@ class Context:
     def set_token_order(self, order: str) -> None:
         """"chunk_aligned" (default, reading R11') or "rank_major" (R11): the global token order the
         plan's chunk ranges index.  Same on every rank; outputs identical, link bytes differ."""
-        _check(_lib.llep_context_set_token_order(self._h, {"rank_major": ORDER_RANK_MAJOR,
-                                                          "chunk_aligned": ORDER_CHUNK_ALIGNED}[order]))
+        code = {"rank_major": ORDER_RANK_MAJOR, "chunk_aligned": ORDER_CHUNK_ALIGNED}[order]
+        if self.P > 1:   # collective: every rank must address peers' rows with the same order
+            import torch.distributed as dist
+            allo: list = [None] * self.P
+            dist.all_gather_object(allo, code, group=self.group)
+            if len(set(allo)) != 1:
+                raise LLEPError(1, f"llep_context_set_token_order: ranks disagree on the token order ({allo})")
+        _check(_lib.llep_context_set_token_order(self._h, code))
 
     def set_memory_cap(self, nbytes: int) -> None:
         _check(_lib.llep_context_set_memory_cap(self._h, int(nbytes)))

@@ -340,6 +340,9 @@ llep_status llep_context_stats(llep_context *ctx, llep_stats *out, int32_t reset
  *   LLEP_DBG_GROUPS       int32 [G*8]        (expert, weight slot (-1-f = foreign f), row_base,
  *                                             n_rows, mblk_start, 0, 0, 0), G = my_groups
  *   LLEP_DBG_RECV_X       bf16 [rows*D]      LLEP_DBG_ACT bf16 [rows*H]   LLEP_DBG_Y bf16 [rows*D]
+ *                         (RECV_X: every received row; under the opt-in LLEP_GATHER=1 the rows this
+ *                         rank sends to itself in all-local m-blocks are read from x instead and
+ *                         are not in RECV_X)
  *   LLEP_DBG_LOCAL_RANK   int32 [B*K]  (r_j: rank of slot j among this rank's slots of ids[j]) */
 enum {
   LLEP_DBG_LOAD_MATRIX = 1,

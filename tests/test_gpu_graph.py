@@ -97,3 +97,21 @@ def test_layer_small_and_empty_batches_p1(L):
         assert torch.equal(a, b), B
     ctx.check()
     ctx.close()
+
+
+@pytest.mark.parametrize("P,cfg,n,seed,port", [(2, "tiny", 24, 101, 29671), (4, "tiny", 24, 202, 29672),
+                                               (8, "tiny", 16, 303, 29673), (4, "g20", 6, 404, 29674)])
+def test_layer_call_fuzz_processes(L, tmp_path, P, cfg, n, seed, port):
+    """Random skews and planner parameters (spills, force-assigns, λ fallbacks, EP): the capture-safe
+    call == the two-call path bit for bit on every rank, and the cases exercise every plan kind."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    cmd = [sys.executable, os.path.join(HERE, "mp_layer_fuzz_worker.py"), str(P), cfg, str(n), str(seed), str(tmp_path)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = [np.load(os.path.join(tmp_path, f"fuzz{p}.npz")) for p in range(P)]
+    for p in range(P):
+        assert res[p]["same"].all(), (p, np.nonzero(~res[p]["same"])[0], res[p]["info"][~res[p]["same"]])
+    info = res[0]["info"]
+    assert (info[:, 7] > 0).any()                        # some plans spill (weight transfers)
+    if n >= 16:
+        assert (info[:, 9] > 0).any()                    # and some fall back to EP (λ test)

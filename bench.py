@@ -226,6 +226,45 @@ def run_graph(L, ctx, inputs, ref_out, steps, warmup, world):
                     "replayed; inputs resident"}
 
 
+def run_p8_emulation(L, base, hot, nhot, reps=4):
+    """GEMM-only critical-rank emulation of the 8-GPU layer on this one GPU (tools/emulate_p8.py): the
+    plans of all 8 ranks from the synthetic per-rank counts, the most loaded rank's grouped GEMM1 + GEMM2
+    under EP and under LLEP timed here (alternating, median), NVLink time MODELLED from the plan (dispatch +
+    combine rows, weight tree, 900 GB/s per direction).  Context for the north-star ratio, not the metric."""
+    import statistics
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import emulate_p8 as E
+    P = 8
+    sh = W.LayerShape(base.n_experts, base.top_k, base.d_model, base.d_ff, base.tokens_per_rank, P)
+    M = sh.experts_per_rank
+    cnt = W.slot_counts(sh.n_experts, sh.tokens_per_rank * sh.top_k, hot, nhot)
+    res, g = {}, {}
+    for mode in ("ep", "llep"):
+        plan = L.plan_host((cnt * P).tolist(), P, 1.0, 1024, 1.3, ep=(mode == "ep"))
+        per_rank = [sum(E.rank_groups(plan, r, M)) for r in range(P)]
+        crit = int(np.argmax(per_rank))
+        rows = E.rank_groups(plan, crit, M)
+        g[mode] = E.Gemms(rows, sh.d_model, sh.d_ff)
+        res[mode] = {"critical_rank": crit, "rows": int(sum(rows)), "transfers": len(plan.transfers),
+                     "link_ms_modelled": 1e3 * E.link_seconds(plan, cnt, sh.d_model, sh.d_ff, M, P), "ms": []}
+    for m in ("ep", "llep"):
+        g[m].run_ms(1)
+    for _ in range(reps):
+        for m in ("ep", "llep"):
+            res[m]["ms"].append(g[m].run_ms(2))
+    for m in ("ep", "llep"):
+        res[m]["gemm_ms"] = statistics.median(res[m].pop("ms"))
+    del g
+    torch.cuda.empty_cache()
+    return {"world": P, "ep": res["ep"], "llep": res["llep"],
+            "gemm_speedup": res["ep"]["gemm_ms"] / res["llep"]["gemm_ms"],
+            "modelled_layer_speedup": (res["ep"]["gemm_ms"] + res["ep"]["link_ms_modelled"]) /
+                                      (res["llep"]["gemm_ms"] + res["llep"]["link_ms_modelled"]),
+            "note": "GEMM-only critical-rank emulation on ONE GPU (NVLink time modelled at 900 GB/s per "
+                    "direction, not executed): context for the north-star >= 3x, not a multi-GPU measurement"}
+
+
 def link_bytes(plan, C, D, H, aligned=True):
     """Bytes each device sends / receives over NVLink in the three exchange phases of one layer step,
     from the replicated plan and the [P, N] load matrix (bench-side accounting):
@@ -593,6 +632,12 @@ def gpu_main(args):
         bwd_ms, train_ms = run_backward(L, ll_ctx, shape, inputs, max(3, args.steps // 2), 3, world, SEED)
     ll_ctx.close()
     router = run_router(L, shape, x, max(10, args.steps), 3)
+    emulation = None
+    if world == 1 and not args.no_emulation and hot is not None:
+        try:
+            emulation = run_p8_emulation(L, base, hot, args.nhot)
+        except Exception as err:   # context only: never cost the line
+            emulation = {"error": f"{type(err).__name__}: {err}"[:300]}
     cublas = run_cublas_ref(shape, int(ll["my_rows"]), max(10, args.steps)) if world == 1 else None
     trace = run_trace(L, shape, rank, local, world, group, args.trace, args.steps, args.warmup) \
         if args.trace else None
@@ -728,6 +773,8 @@ def gpu_main(args):
                                                    "llep_moe_backward_saved (no GU recompute): one training step "
                                                    "of the layer; tflops over 18·D·H per routed row"}}
     line["graph"] = graph
+    if emulation:
+        line["p8_critical_rank_emulation"] = emulation
     router["frac_hbm"] = router["gbs"] / peaks["hbm_gbs"]
     line["router"] = router
     if trace:
@@ -814,6 +861,8 @@ def main():
     ap.add_argument("--no-backward", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-distinct", action="store_true", help="skip the distinct-ids routing variant")
+    ap.add_argument("--no-emulation", action="store_true",
+                    help="skip the GEMM-only P=8 critical-rank emulation (N=1 only)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -100,7 +100,8 @@ def test_layer_small_and_empty_batches_p1(L):
 
 
 @pytest.mark.parametrize("P,cfg,n,seed,port", [(2, "tiny", 24, 101, 29671), (4, "tiny", 24, 202, 29672),
-                                               (8, "tiny", 16, 303, 29673), (4, "g20", 6, 404, 29674)])
+                                               (8, "tiny", 16, 303, 29673), (4, "g20", 6, 404, 29674),
+                                               (8, "dsv3", 3, 505, 29675)])
 def test_layer_call_fuzz_processes(L, tmp_path, P, cfg, n, seed, port):
     """Random skews and planner parameters (spills, force-assigns, λ fallbacks, EP): the capture-safe
     call == the two-call path bit for bit on every rank, and the cases exercise every plan kind."""

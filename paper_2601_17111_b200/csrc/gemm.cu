@@ -451,8 +451,14 @@ struct Cfg2 {
 };
 
 
-template <int BN, int MODE, int KSUB>
+// MC = 1: clusters of one CTA pair.  MC = 2: clusters of two CTA pairs that compute the two adjacent N
+// tiles (nb = 2j, 2j+1) of the same m-block in lockstep: the activation (A) tile they share is loaded ONCE
+// from L2 and multicast to both pairs (each of the four CTAs issues one of the two 64-deep K sub-tiles of
+// its row half, for itself and its counterpart in the other pair), halving the A operand's L2 reads; a
+// stage is refilled only when both pairs' MMAs released it (empty barriers count one commit per pair).
+template <int BN, int MODE, int KSUB, int MC>
 __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(const __grid_constant__ GemmParams p) {
+  static_assert(MC == 1 || (MC == 2 && KSUB == 2), "A multicast splits a stage's two K sub-tiles over the pairs");
   using C = Cfg2<BN, KSUB, (MODE == 0 || MODE == 3) ? kXchgBytes : kStoreStageBytes>;
   constexpr int KST = BK * KSUB;                 // K per pipeline stage
   constexpr int S = C::STAGES;
@@ -472,13 +478,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
   float *xchg = reinterpret_cast<float *>(smem + S * C::STAGE + 256);   // mode 0 half tiles
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t crank = cluster_ctarank();
+  const uint32_t ccr = cluster_ctarank();           // rank in the cluster (2 * MC CTAs)
+  const uint32_t crank = ccr & 1u;                  // rank in the CTA pair
+  const uint32_t lead = ccr & ~1u;                  // the pair's leader: issues the MMAs, owns the barriers
+  const int cpair = (int)(ccr >> 1);                // which pair of the cluster (MC = 2: N tile 2j + cpair)
   const bool leader = crank == 0;
   const int n_groups = p.n_groups_dev ? *p.n_groups_dev : p.n_groups_host;
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(smem_u32(full + i), 1);
-      mbar_init(smem_u32(empty + i), 1);
+      mbar_init(smem_u32(empty + i), MC);        // one MMA-completion commit per pair sharing the stage
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(tfull + i), 1);
@@ -507,7 +516,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
     total_tiles = (last.mblk_start + (last.n_rows + TM - 1) / TM) * p.n_ntiles;
   }
   const int nk = (p.kdim + KST - 1) / KST;
-  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  // work units: one tile per pair (MC = 1) or the tile pair (2j, 2j+1) of an m-block per cluster (MC = 2)
+  const int unit0 = blockIdx.x / (2 * MC), n_units = gridDim.x / (2 * MC);
+  const int total_units = total_tiles / MC;
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer (both CTAs)
@@ -523,7 +534,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
     uint32_t phase = 0;
     uint32_t seen = 0;   // sources whose arrival lane 0 already acquired
     const uint32_t wep = p.ep ? p.ep[kEpWeight] : 0u, aep = p.ep ? p.ep[kEpArrive] : 0u;
-    for (int t = pair; t < total_tiles; t += n_pairs) {
+    for (int u = unit0; u < total_units; u += n_units) {
+      const int t = u * MC + cpair;
       TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
       ti.swap = p.swap && ti.row_end - ti.row0 <= 64;
       const CUtensorMap *wm = ti.wslot >= 0 ? &p.tmW0 : &p.tmW1;
@@ -559,7 +571,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
           mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const int nsub = min(SWK, (p.kdim - kb * SWK * BK + BK - 1) / BK);
           const uint32_t fl = smem_u32(full + stage);
-          const uint32_t fb = mapa_shared(fl, 0);
+          const uint32_t fb = mapa_shared(fl, lead);
           if (lane == 0) {
             if (leader) mbar_expect_tx(fl, 2 * nsub * (BM * 128 + 32 * 128));
             for (int s2 = 0; s2 < nsub; ++s2) {
@@ -589,13 +601,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
         mbar_wait(smem_u32(empty + stage), phase ^ 1);
         const int nsub = min(KSUB, (p.kdim - kb * KST + BK - 1) / BK);   // skip all-OOB sub-tiles
         const uint32_t fl = smem_u32(full + stage);
-        const uint32_t fb = mapa_shared(fl, 0);
+        const uint32_t fb = mapa_shared(fl, lead);
         if (lane == 0) {
           if (leader) mbar_expect_tx(fl, 2 * nsub * (C::STAGE / KSUB));
           for (int s2 = 0; s2 < nsub; ++s2) {
-            if (!gat)
-              tma_load_2d_pair(smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128)), &p.tmA, fb,
-                               (kb * KSUB + s2) * BK, ti.row0 + (int)crank * (ti.half ? BM / 2 : BM), pol_act);
+            const uint32_t adst = smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128));
+            const int arow = ti.row0 + (int)crank * (ti.half ? BM / 2 : BM);
+            if (MC == 2) {   // sub-tile s2 of this row half, issued by pair s2, into both pairs' CTAs
+              if (s2 == cpair)
+                tma_load_2d_pair_mc(adst, &p.tmA, fb, (kb * KSUB + s2) * BK, arow,
+                                    (uint16_t)((1u << crank) | (1u << (2 + crank))), pol_act);
+            } else if (!gat) {
+              tma_load_2d_pair(adst, &p.tmA, fb, (kb * KSUB + s2) * BK, arow, pol_act);
+            }
             tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES + s2 * ((BN / 2) * 128)), wm, fb,
                              (kb * KSUB + s2) * BK, brow, ti.small ? pol_first : pol_last);
           }
@@ -626,7 +644,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = pair; t < total_tiles; t += n_pairs, ++it) {
+      const uint16_t m_empty = MC == 2 ? 0xF : 0x3, m_full = (uint16_t)(0x3u << lead);
+      for (int u = unit0; u < total_units; u += n_units, ++it) {
+        const int t = u * MC + cpair;
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
@@ -654,13 +674,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
                                 (kb | s2 | kk) != 0);
               }
             }
-            tc_commit_pair_w(smem_u32(empty + stage));
+            tc_commit_pair_mask(smem_u32(empty + stage), m_empty);
             if (++stage == S) {
               stage = 0;
               phase ^= 1;
             }
           }
-          tc_commit_pair_w(smem_u32(tfull + acc));
+          tc_commit_pair_mask(smem_u32(tfull + acc), m_full);
           continue;
         }
         for (int kb = 0; kb < nk; ++kb) {
@@ -681,20 +701,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
                               (kb | s2 | kk) != 0);
             }
           }
-          tc_commit_pair_w(smem_u32(empty + stage));
+          tc_commit_pair_mask(smem_u32(empty + stage), m_empty);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit_pair_w(smem_u32(tfull + acc));
+        tc_commit_pair_mask(smem_u32(tfull + acc), m_full);
       }
     }
   } else {
     // ------------------------------------------------------------------ epilogue (both CTAs)
     const int q = warp & 3;
     int it = 0;
-    for (int t = pair; t < total_tiles; t += n_pairs, ++it) {
+    for (int u = unit0; u < total_units; u += n_units, ++it) {
+      const int t = u * MC + cpair;
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
@@ -987,7 +1008,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(tempty + acc), 0));
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(tempty + acc), lead));
       __syncwarp();   // reconverge: named barriers (bar.sync) that follow require converged warps
     }
   }
@@ -1065,15 +1086,23 @@ llep_status launch(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
 template <int BN, int MODE, int KSUB = LLEP_FWD_KSUB>
 llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
   using C = Cfg2<BN, KSUB, (MODE == 0 || MODE == 3) ? kXchgBytes : kStoreStageBytes>;
-  auto kern = grouped_gemm_2cta_kernel<BN, MODE, KSUB>;
+  // opt-in (LLEP_GEMM_MC=2): two-pair clusters with the A tile multicast when the N tiles pair up.
+  // Correct (bit-identical) and 25 % fewer L2 bytes, but clusters of 4 fit only 132 of the 148 SMs
+  // (GPCs' SM counts are not multiples of 4), which costs more than the multicast saves: G120 layer
+  // step +12 %, Q3 +7 % (profiles/r02_ab_multicast.txt).  Default: single pairs on all 148 SMs.
+  const int n_nt = (g.nout + (MODE != 1 ? BN / 2 : BN) - 1) / (MODE != 1 ? BN / 2 : BN);
+  const char *mce = getenv("LLEP_GEMM_MC");
+  const int mc = (KSUB == 2 && n_nt % 2 == 0 && !g.rtok && mce && atoi(mce) == 2) ? 2 : 1;
+  auto kern = mc == 2 ? grouped_gemm_2cta_kernel<BN, MODE, KSUB, (KSUB == 2 ? 2 : 1)>
+                      : grouped_gemm_2cta_kernel<BN, MODE, KSUB, 1>;
   if (!g.sched) {   // the pair kernels walk the layout's interleaved m-block schedule
     set_error("pair GEMM needs the m-block schedule (LLEP_GEMM_GROUP_ORDER applies to the 1-CTA kernels)");
     return LLEP_ERR_INVALID;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[mc - 1]) {
     LLEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr_set = true;
+    attr_set[mc - 1] = true;
   }
   const int box_w = BN / 2;
   const int wrows = MODE != 1 ? 2 * g.nout : g.nout;
@@ -1104,20 +1133,33 @@ llep_status launch_pair(const GemmArgs &g, GemmParams &prm, cudaStream_t s) {
   prm.wup_off = MODE != 1 ? g.nout : 0;
   prm.n_ntiles = (g.nout + (MODE != 1 ? BN / 2 : BN) - 1) / (MODE != 1 ? BN / 2 : BN);
   cudaLaunchConfig_t cfg = {};
-  int grid = g.num_sms & ~1;
+  int grid = g.num_sms & ~(2 * mc - 1);
   if (const char *gp = getenv("LLEP_GEMM_PAIRS"))   // measurement only: fewer CTA pairs (per-pair rates)
-    grid = 2 * std::max(1, std::min(grid / 2, atoi(gp)));
+    grid = 2 * mc * std::max(1, std::min(grid / (2 * mc), atoi(gp) / mc));
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = 2 * mc;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (mc == 2) {
+    // a persistent grid must be co-resident: clusters of 4 need 4 free SMs in one GPC, so size the grid
+    // by the occupancy API (GPCs whose SM count is not a multiple of 4 lose their remainder SMs)
+    static int max_clusters = 0;
+    if (!max_clusters) {
+      cudaLaunchConfig_t q = cfg;
+      q.gridDim = dim3((unsigned)(g.num_sms & ~3));
+      if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &q) != cudaSuccess || max_clusters < 1)
+        max_clusters = (g.num_sms & ~3) / 4;
+      (void)cudaGetLastError();
+    }
+    cfg.gridDim = dim3((unsigned)std::min(grid, 4 * max_clusters));
+  }
   LLEP_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
   return LLEP_OK;
 }

@@ -157,6 +157,25 @@ __device__ __forceinline__ void tc_mma_pair_w(uint32_t d_tmem, uint64_t adesc, u
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// MMA-completion arrive on the barrier at offset `bar` of every CTA in `mask` (cluster ranks)
+__device__ __forceinline__ void tc_commit_pair_mask(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+      ::"r"(bar), "h"(mask)
+      : "memory");
+}
+// TMA box load on a CTA pair, multicast to the cluster CTAs in `mask`; completion bytes are signalled
+// on the barrier at `leader_bar`'s offset in each destination's pair leader
+__device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap *map, uint32_t leader_bar,
+                                                    int c0, int c1, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar), "h"(mask), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tc_commit_pair_w(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

@@ -577,3 +577,29 @@ def test_token_orders_same_outputs_different_rows(L, tmp_path):
     for a, b in zip(outs["rank_major"], outs["chunk_aligned"]):
         assert np.array_equal(a, b)
     assert dst["chunk_aligned"] > dst["rank_major"], dst
+
+
+@pytest.mark.parametrize("cfg", ["g20", "q3"])
+def test_multicast_clusters_bitwise_equal(L, cfg):
+    """Opt-in two-pair clusters with the activation tile multicast (LLEP_GEMM_MC=2) give bit-identical
+    layer outputs and saved [g | u] to the default single-pair kernels: same tiles, same MMAs, same K order."""
+    base = W.CONFIGS[cfg]
+    B = min(base.tokens_per_rank, 4096)
+    sh = W.LayerShape(base.n_experts, base.top_k, base.d_model, base.d_ff, B, 1)
+    x, ids, gates, w13, w2, ids_np, g_np = LC.rank_inputs(sh, 0, 95, 1, 17, "cuda")
+    ctx = L.Context(sh.n_experts, sh.top_k, sh.d_model, sh.d_ff, 1, 0, 0, B)
+    res = {}
+    for mc in ("1", "2"):
+        os.environ["LLEP_GEMM_MC"] = mc
+        try:
+            plan, req = ctx.prepare(ids)
+            out = ctx.forward(x, ids, gates, w13, w2, plan)
+            gu = torch.zeros((int(req.rows_needed), 2 * sh.d_ff), dtype=torch.bfloat16, device="cuda")
+            out2, gu = ctx.forward_train(x, ids, gates, w13, w2, plan, gu=gu)
+            torch.cuda.synchronize()
+            res[mc] = (out.cpu(), out2.cpu(), gu.cpu())
+        finally:
+            os.environ.pop("LLEP_GEMM_MC", None)
+    for a, b in zip(res["1"], res["2"]):
+        assert torch.equal(a, b)
+    ctx.close()

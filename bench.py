@@ -459,8 +459,9 @@ def run_cublas_ref(shape, rows, steps):
 
 def run_e2e(L, ctx, shape, host, dev, steps, warmup, world, ep=False):
     """Public API end to end: every step copies its inputs from pinned host memory (H2D), runs the
-    layer (llep_prepare + llep_moe_forward) and reads the output back (D2H).  Double-buffered: the
-    H2D of step i+1 and the D2H of step i-1 run on copy streams while step i computes."""
+    layer through llep_moe_layer (the one-call path: no host synchronisation, so the host keeps the
+    copy streams fed) and reads the output back (D2H).  Double-buffered: the H2D of step i+1 and the
+    D2H of step i-1 run on copy streams while step i computes."""
     import torch
     x_h, ids_h, g_h = host
     _, _, _, w13, w2 = dev
@@ -493,7 +494,7 @@ def run_e2e(L, ctx, shape, host, dev, steps, warmup, world, ep=False):
         b = i % nb
         comp.wait_event(ev_h2d[b])
         comp.wait_event(ev_d2h[b])              # D2H of step i-2 done with outs[b]
-        ctx(xs[b], idss[b], gs[b], w13, w2, ep=ep, plan_out=plans[b], out=outs[b])
+        ctx.layer(xs[b], idss[b], gs[b], w13, w2, ep=ep, plan_out=plans[b], out=outs[b])
         ev_comp[b].record(comp)
         with torch.cuda.stream(d2h):
             d2h.wait_event(ev_comp[b])
@@ -518,7 +519,9 @@ def run_e2e(L, ctx, shape, host, dev, steps, warmup, world, ep=False):
     ms = max_over_ranks(e0.elapsed_time(e1), world)
     bytes_h2d = x_h.numel() * 2 + ids_h.numel() * 4 + g_h.numel() * 4
     bytes_d2h = outs_h[0].numel() * 2
-    return ms / steps, bytes_h2d, bytes_d2h
+    torch.cuda.synchronize()
+    ctx.check()
+    return ms / steps, bytes_h2d, bytes_d2h, outs_h[(steps - 1) % nb]
 
 
 def cpu_baseline(shape, hot, nhot, budget_s=12.0, max_tokens=65536):
@@ -618,11 +621,12 @@ def gpu_main(args):
     if not args.no_e2e:
         host = (x.cpu().pin_memory(), ids.cpu().pin_memory(), gates.cpu().pin_memory())
         dev_bufs = (torch.empty_like(x), torch.empty_like(ids), torch.empty_like(gates), w13, w2)
-        ms_e2e, h2d, d2h = run_e2e(L, ll_ctx, shape, host, dev_bufs, max(3, args.steps // 2), 2, world)
+        ms_e2e, h2d, d2h, out_h = run_e2e(L, ll_ctx, shape, host, dev_bufs, max(3, args.steps), 2, world)
         e2e = {"value": world * B / (ms_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
+               "output_equals_device_path_bitwise": bool(torch.equal(out_h, ll_out.cpu())),
                "note": "pinned host -> device inputs and device -> host output every step, "
-                       "double-buffered on copy streams"}
+                       "double-buffered on copy streams; layer via llep_moe_layer (no host sync)"}
     try:
         graph = run_graph(L, ll_ctx, inputs, ll_out, args.steps, args.warmup, world)
     except Exception as err:   # a capture problem must not cost the rest of the line

@@ -18,7 +18,13 @@
 // The default kernels are the CTA-pair versions (grouped_gemm_2cta_kernel, cta_group::2, groups
 // 256-row aligned): M=256 tiles, M=128 pair MMAs for blocks with <= 128 rows left, and SWAPPED tiles
 // for groups of <= 64 rows (D = W·Xᵀ: M=256 over weight rows, N=64 over the group's tokens, three
-// K sub-tiles per stage) -- at P=1 those are the cold experts, whose cost is streaming their weights.
+// K sub-tiles per stage) -- at P=1 those are the cold experts, whose cost is streaming their weights
+// (bounded by the ~60-70 GB/s of HBM ingest one SM sustains, profiles/r02_cold_stream_limit.txt).
+// Producers wait per foreign group for its weight flag and per m-block for the dispatch arrival flags
+// of the sources of its rows (row f2), so GEMM1 starts before the slowest peer has finished sending.
+// A/B-only variants of the pair kernel: MC = 2 (LLEP_GEMM_MC=2: two pairs per cluster sharing the
+// activation tile by TMA multicast) and the TMA gather4 of this rank's own rows (LLEP_GATHER=1); both
+// are bit-identical and measured slower.
 // Backward GEMMs (gemm_bwd_*_kernel, row f1) follow at the end of the file.
 #include <cuda.h>
 #include <cuda_bf16.h>

@@ -1,6 +1,7 @@
 """Fuzz of the capture-safe layer call against the two-call path at P > 1 (processes sharing one GPU):
 random skews (1/4/16 hot experts, sampled or exact counts, balanced), random planner parameters (α, m, λ)
-so that spills, force-assigns and λ fallbacks all occur, LLEP and EP; per case the direct llep_moe_layer
+so that spills, force-assigns and λ fallbacks all occur, LLEP and EP, and ragged batches (each rank its own
+token count, some ranks empty); per case the direct llep_moe_layer
 output must equal the two-call output bit for bit and leave no device error.
 
     python mp_layer_fuzz_worker.py P CFG N_CASES SEED OUTDIR    -> OUTDIR/fuzz{p}.npz"""
@@ -38,12 +39,18 @@ def worker(rank, P, cfg, n_cases, seed, outdir):
         m = int(rng.choice([1, 16, 256, 1024]))
         lam = float(rng.choice([1.0, 1.3, 3.0]))
         ep = bool(rng.integers(0, 4) == 0)
+        ragged = bool(rng.integers(0, 3) == 0)   # every third case: a different batch per rank, some empty
         ids = W.routing_ids(sh, rank, None if pct == 0 else pct, nhot, seed + 7 * i, sampled=sampled)
         ids = torch.from_numpy(((ids + shift) % sh.n_experts).astype(np.int32)).to(d)
         g = torch.from_numpy(W.gate_weights(B, sh.top_k, rank, seed + i)).to(d)
-        a = ctx(x, ids, g, w13, w2, alpha, m, lam, ep=ep).clone()
+        xb = x
+        if ragged:
+            r_rng = np.random.default_rng([seed, i, rank])
+            Br = int(r_rng.choice([0, 1, 7, B // 3, B]))
+            xb, ids, g = x[:Br].contiguous(), ids[:Br].contiguous(), g[:Br].contiguous()
+        a = ctx(xb, ids, g, w13, w2, alpha, m, lam, ep=ep).clone()
         req = ctx.last_req
-        b = ctx.layer(x, ids, g, w13, w2, alpha, m, lam, ep=ep)
+        b = ctx.layer(xb, ids, g, w13, w2, alpha, m, lam, ep=ep)
         torch.cuda.synchronize()
         ctx.check()
         same.append(bool(torch.equal(a, b)))

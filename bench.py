@@ -53,14 +53,15 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device = device
-        self.rows = []
+        self.rows = []          # (host time of arrival, fields)
         self.proc = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
-                 "-i", str(self.device), "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-i", str(self.device), "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except OSError:
@@ -70,7 +71,11 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) == len(self.FIELDS):
-                self.rows.append(parts)
+                self.rows.append((time.perf_counter(), parts))
+
+    def window(self, t0: float, t1: float):
+        """Host times bracketing the timed region (barrier + synchronize on both sides)."""
+        self.t0, self.t1 = t0, t1
 
     def stop(self):
         if not self.proc:
@@ -81,11 +86,17 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:]) if v.lower() == "active"})
+        rows = [r for (t, r) in self.rows]
+        if self.t0 is not None:
+            # samples taken during the timed region (nvidia-smi prints ~tens of ms after sampling);
+            # the sampler runs from before the warm-up so a short region still gets samples
+            inside = [r for (t, r) in self.rows if self.t0 <= t <= self.t1 + 0.05]
+            rows = inside if inside else [r for (t, r) in self.rows if t <= self.t1 + 0.05][-3:]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({n for r in rows for n, v in zip(self.NAMES, r[2:]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows), "sampling_ms": 20}
 
 
 def dist_setup(n_gpus: int):
@@ -146,6 +157,8 @@ def run_mode(L, shape, rank, local, world, group, inputs, ep: bool, steps: int, 
         ctx.set_memory_cap(int(mem_cap_gb * 1e9) - torch.cuda.memory_allocated())
     out = torch.empty_like(x)
     plan_buf = torch.empty(L.plan_bytes(shape.n_experts, world), dtype=torch.uint8, device=x.device)
+    if clocks:
+        clocks.start()   # before the warm-up: nvidia-smi needs a moment before its first sample
     try:
         for _ in range(warmup):
             ctx(x, ids, gates, w13, w2, ep=ep, plan_out=plan_buf, out=out)
@@ -153,12 +166,13 @@ def run_mode(L, shape, rank, local, world, group, inputs, ep: bool, steps: int, 
         if err.code != 4:
             raise
         ctx.close()
+        if clocks:
+            clocks.stop()
         return {"oom": True, "error": str(err), "ctx": None, "out": None}
     ctx.set_timing(True)
     ctx.stats(reset=True)
     barrier(world)
-    if clocks:
-        clocks.start()
+    t_host0 = time.perf_counter()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
@@ -166,6 +180,8 @@ def run_mode(L, shape, rank, local, world, group, inputs, ep: bool, steps: int, 
         ctx(x, ids, gates, w13, w2, ep=ep, plan_out=plan_buf, out=out)
     e1.record(s)
     barrier(world)
+    if clocks:
+        clocks.window(t_host0, time.perf_counter())
     clk = clocks.stop() if clocks else None
     ms = e0.elapsed_time(e1)
     st = ctx.stats(reset=True)

@@ -45,19 +45,46 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
+    """SM clock + throttle reasons sampled every 5 ms from a host thread (NVML in process; nvidia-smi
+    -lms 20 as the fallback) from before the warm-up to after the timed region; stop() keeps the samples
+    inside the host window of the timed region (barrier + synchronize on both sides)."""
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap"]
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    NVML_BITS = [0x8, 0x40, 0x20, 0x4]   # nvmlClocksEventReason{HwSlowdown, HwThermal, SwThermal, SwPowerCap}
 
     def __init__(self, device: int):
         self.device = device
-        self.rows = []          # (host time of arrival, fields)
+        self.rows = []          # (host time of the sample, fields)
         self.proc = None
+        self.nvml = None
+        self.period_ms = 5
         self.t0 = self.t1 = None
+        self.halt = threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+        try:
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID("GPU-" + uuid)
+        except pynvml.NVMLError:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.device)
 
     def start(self):
+        try:
+            nv, h = self._nvml_handle()
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.nvml = (nv, h, mx)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
+        self.period_ms = 20
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
@@ -66,6 +93,15 @@ class ClockSampler:
             self.thread.start()
         except OSError:
             self.proc = None
+
+    def _poll(self):
+        nv, h, mx = self.nvml
+        while not self.halt.is_set():
+            t = time.perf_counter()
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append((t, [str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in self.NVML_BITS]))
+            time.sleep(self.period_ms / 1000)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -78,25 +114,30 @@ class ClockSampler:
         self.t0, self.t1 = t0, t1
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
+        if not self.proc and not self.nvml:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml and nvidia-smi unavailable"], "samples": 0}
+        if self.nvml:
+            self.halt.set()
+            self.thread.join(timeout=5)
+            late = 0.0
+        else:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            late = 0.05   # nvidia-smi prints ~tens of ms after sampling
         rows = [r for (t, r) in self.rows]
         if self.t0 is not None:
-            # samples taken during the timed region (nvidia-smi prints ~tens of ms after sampling);
-            # the sampler runs from before the warm-up so a short region still gets samples
-            inside = [r for (t, r) in self.rows if self.t0 <= t <= self.t1 + 0.05]
-            rows = inside if inside else [r for (t, r) in self.rows if t <= self.t1 + 0.05][-3:]
+            inside = [r for (t, r) in self.rows if self.t0 <= t <= self.t1 + late]
+            rows = inside if inside else [r for (t, r) in self.rows if t <= self.t1 + late][-3:]
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         reasons = sorted({n for r in rows for n, v in zip(self.NAMES, r[2:]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows), "sampling_ms": 20}
+                "reasons": reasons, "samples": len(rows), "sampling_ms": self.period_ms,
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def dist_setup(n_gpus: int):

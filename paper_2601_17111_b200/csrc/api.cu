@@ -992,7 +992,7 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   mark(c, 4, s);
   if (any_copy) LLEP_CUDA(cudaEventRecord(c->ev_join, c->side));
   // a6: dispatch (gather-on-send into every destination's receive rows)
-  DispatchArgs da;
+  DispatchArgs da{};
   da.x = x;
   da.ids = ids;
   da.w = topk_w;
@@ -1250,7 +1250,7 @@ static llep_status moe_backward(llep_context *c, const uint16_t *x, const int32_
   }
   if ((st = push_weights(c, w13, w2, s, &any_copy)) != LLEP_OK) return st;
   if (any_copy) LLEP_CUDA(cudaEventRecord(c->ev_join, c->side));
-  DispatchArgs da;
+  DispatchArgs da{};
   da.x = x;
   da.ids = ids;
   da.w = topk_w;

@@ -1509,11 +1509,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_bwd_kernel(const __grid_
 constexpr int kPairA = BM * BK * 2;        // 16 KB per CTA
 constexpr int kPairB = 128 * BK * 2;       // 16 KB per CTA (half of N)
 constexpr int kPairStage = kPairA + kPairB;
+// pair weight-gradient kernel: operand pipeline stages (64-deep, 32 KB each) and fp32 staging buffers
+// (TMA stores in flight).  5 + 3 beat round 1's 4 + 4 by 6-8 % at base clocks on the P=8 critical-rank
+// layout and at P=1 (tensor pipe 78 -> 84.5 %, profiles/r02_ab_wgrad_stages.txt)
 #ifndef LLEP_WG_NSTG
-#define LLEP_WG_NSTG 4    // pair weight-gradient epilogue: fp32 staging buffers (TMA stores in flight)
+#define LLEP_WG_NSTG 3
 #endif
 #ifndef LLEP_WG_STAGES
-#define LLEP_WG_STAGES 4  // pair weight-gradient kernel: operand pipeline stages
+#define LLEP_WG_STAGES 5
 #endif
 constexpr int kPairNStg = LLEP_WG_NSTG;
 #ifndef LLEP_BWD_KSUB

@@ -20,6 +20,7 @@ groups, rb = [], 0
 for i, n in enumerate(sizes):
     groups.append((i, rb, n))
     rb += (n + 255) // 256 * 256
+torch.manual_seed(0)
 a = torch.randn(rb, mdim, device="cuda").to(torch.bfloat16)
 b = torch.randn(rb, nout, device="cuda").to(torch.bfloat16)
 for (i, r0, n) in groups:
@@ -43,5 +44,7 @@ for _ in range(10):   # 4 back-to-back launches per event pair: the host-side pr
 ms = statistics.median(ts)
 flops = 2.0 * mdim * nout * sum(sizes)
 wbytes = len(groups) * mdim * nout * 4
+import hashlib  # noqa: E402
+digest = hashlib.sha1(out.cpu().numpy().tobytes()).hexdigest()[:12]   # A/B variants must agree bitwise
 print(f"{which} mdim={mdim} nout={nout} pair={pair}: {ms:.3f} ms, {flops / ms / 1e9:.0f} TFLOP/s, "
-      f"output {wbytes / 1e9:.2f} GB -> {wbytes / ms / 1e6:.0f} GB/s", flush=True)
+      f"output {wbytes / 1e9:.2f} GB -> {wbytes / ms / 1e6:.0f} GB/s, sha1 {digest}", flush=True)

@@ -75,6 +75,26 @@ __host__ __device__ inline int wgrad_splits(int n_rows, int tiles_per_split, int
   const int cap = padded / 1024;                                       // >= 1024 rows per split
   if (want > cap) want = cap;
   if (want < 1) want = 1;
+#ifndef LLEP_WG_WAVEFIT
+#define LLEP_WG_WAVEFIT 1
+#endif
+  if (LLEP_WG_WAVEFIT) {
+    // the tiles are scheduled statically over the units, so a last wave that is only partly full
+    // leaves units idle for one (long) tile: take up to 2x the splits if that fills the waves >= 2 %
+    // better (waves per split, ceil(tiles / units) / splits).  G120 P=8 dW13: 276 tiles per split on
+    // 74 CTA pairs -> 2 splits = 7.46 waves run as 8, 4 splits = 14.92 as 15: dW13 + its reduce
+    // -0.3..-2 % (P=8 layout) and -3 % (P=1) at base clocks (profiles/r02_ab_wgrad_wavefit.txt); the
+    // small groups' tiles that follow already fill most of the idle tail
+    const int w0 = want;
+    float best = (float)((tiles_per_split * w0 + num_sms - 1) / num_sms) / w0;
+    for (int sp = w0 + 1; sp <= 2 * w0 && sp <= cap; ++sp) {
+      const float c = (float)((tiles_per_split * sp + num_sms - 1) / num_sms) / sp;
+      if (c < 0.98f * best) {
+        best = c;
+        want = sp;
+      }
+    }
+  }
   const int ks = ((padded + want - 1) / want + 255) / 256 * 256;       // 256-row aligned K range
   return (padded + ks - 1) / ks;
 }

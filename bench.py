@@ -809,8 +809,8 @@ def gpu_main(args):
                 if world == 1 and st["ms"]["dispatch"] > 0 else None,
                 "peak": peaks["hbm_gbs"],
                 "note": "algorithmic bytes / phase time (P=1: all rows local); peak = the 1:1 copy figure.  The "
-                        "dispatch is a 1:4 read:write mix: torch writes at 3.8 TB/s with fill_ on this GPU "
-                        "(profiles/r02_write_mix_probe.jsonl), the ceiling for its dispatch_write_gbs"},
+                        "dispatch is a 1:4 read:write mix: a bare kernel doing that exact mix runs at 5.6-5.8 "
+                        "TB/s of reads + writes (profiles/r02_write_probe.jsonl), pure writes at 5.9-7.0"},
         "nvlink": {"llep": links, "ep": links_ep,
                    "dispatch_weights_gbs": (max(links["dispatch"]["max_egress_bytes"], links["dispatch"]["max_ingress_bytes"])
                                             + max(links["weights"]["max_egress_bytes"], links["weights"]["max_ingress_bytes"]))

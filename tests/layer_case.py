@@ -18,6 +18,14 @@ TOL_MAX_REL = 2e-2   # north star: max relative error (reading R21)
 TOL_REL_L2 = 5e-3    # north star: relative L2 error
 
 
+def config_shape(cfg: str) -> W.LayerShape:
+    """A synth.CONFIGS name, or "shape:N,K,D,H,B" for a test-only layer shape (world size set by the caller)."""
+    if cfg.startswith("shape:"):
+        n, k, d, h, b = (int(v) for v in cfg[len("shape:"):].split(","))
+        return W.LayerShape(n, k, d, h, b, 1)
+    return W.CONFIGS[cfg]
+
+
 def rank_inputs(shape: W.LayerShape, rank: int, hot_pct, n_hot: int, seed: int, device, sampled=False):
     import torch
     B, K, D, H, M = shape.tokens_per_rank, shape.top_k, shape.d_model, shape.d_ff, shape.experts_per_rank

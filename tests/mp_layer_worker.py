@@ -1,6 +1,6 @@
 """Spawn P ranks (processes) that share one GPU and run the LLEP and EP layer through the C ABI.
 
-    python mp_layer_worker.py P CFG HOT_PCT N_HOT OUTDIR
+    python mp_layer_worker.py P CFG HOT_PCT N_HOT OUTDIR        (CFG: a synth.CONFIGS name or shape:N,K,D,H,B)
 
 The ranks bootstrap a gloo process group on 127.0.0.1 (plumbing only: it carries the 64-byte CUDA
 IPC handles); all data moves through the library's peer-mapped arenas and device barriers.
@@ -41,7 +41,7 @@ def worker(rank, P, cfg, pct, nhot, outdir, sample):
     dist.init_process_group("gloo", rank=rank, world_size=P)
     dev = int(os.environ.get("LLEP_TEST_DEVICE", "0"))
     torch.cuda.set_device(dev)
-    sh0 = W.CONFIGS[cfg]
+    sh0 = LC.config_shape(cfg)
     sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, P)
     x, ids, gates, w13, w2, _, _ = LC.rank_inputs(sh, rank, None if pct == 0 else pct, nhot, 21, f"cuda:{dev}")
     alpha, m, lam = (float(v) for v in os.environ.get("LLEP_TEST_PARAMS", "1,1024,1.3").split(","))

@@ -117,22 +117,26 @@ def test_backward_g120_p1_sampled(L):
     ctx.close()
 
 
-@pytest.mark.parametrize("P,pct,nhot,params", [
-    (2, 95, 1, (1.0, 16, 1.0)),
-    (4, 30, 1, (1.0, 600, 1.3)),   # force-assigned chunks
+@pytest.mark.parametrize("P,pct,nhot,params,cfg", [
+    (2, 95, 1, (1.0, 16, 1.0), "tiny"),
+    (4, 30, 1, (1.0, 600, 1.3), "tiny"),   # force-assigned chunks
+    # the spilled hot expert holds ~15.6K rows on every device: split-K weight gradients (fp32 partials
+    # summed in fixed order) on the native AND the replica side, then the replicas' partials returned
+    (2, 95, 1, (1.0, 1024, 1.3), "shape:8,2,256,512,8192"),
+    (4, 95, 1, (1.0, 1024, 1.3), "shape:8,2,256,512,8192"),
 ])
-def test_backward_multiprocess(L, tmp_path, P, pct, nhot, params):
+def test_backward_multiprocess(L, tmp_path, P, pct, nhot, params, cfg):
     """P processes on one GPU: dx, dgates on every rank; the native rank's weight gradients include
     the partials its replicas computed and returned."""
     from oracle import backward as O5
     alpha, m, lam = params
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29800 + P + pct),
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29800 + P + pct + (7 if cfg != "tiny" else 0)),
                LLEP_TEST_PARAMS=f"{alpha},{m},{lam}", LLEP_TEST_BWD="1")
-    cmd = [sys.executable, os.path.join(HERE, "mp_layer_worker.py"), str(P), "tiny", str(pct), str(nhot), str(tmp_path)]
+    cmd = [sys.executable, os.path.join(HERE, "mp_layer_worker.py"), str(P), cfg, str(pct), str(nhot), str(tmp_path)]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = [np.load(os.path.join(tmp_path, f"rank{p}.npz")) for p in range(P)]
-    sh0 = W.CONFIGS["tiny"]
+    sh0 = LC.config_shape(cfg)
     sh = W.LayerShape(sh0.n_experts, sh0.top_k, sh0.d_model, sh0.d_ff, sh0.tokens_per_rank, P)
     ws = LC.OracleWeights(sh.d_model, sh.d_ff, 21)
     xs, ids, gs, dos = [], [], [], []

@@ -1063,6 +1063,7 @@ static llep_status moe_forward(llep_context *c, const uint16_t *x, const int32_t
   g1.err = c->err;
   g1.arrive = overlap ? reinterpret_cast<const uint32_t *>(c->arena + c->off_flags) + kArriveFlag0 : nullptr;
   g1.mblk_src = c->mblk_src;
+  g1.src_all = P >= 32 ? 0xffffffffu : (1u << P) - 1u;
   g1.row_src = nullptr;
   g1.peer_slot = nullptr;
   g1.num_sms = c->num_sms;

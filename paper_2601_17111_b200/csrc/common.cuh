@@ -292,6 +292,7 @@ struct GemmArgs {
   const uint32_t *arrive;    // row f2: this rank's dispatch arrival flags [P] (nullptr: rows resident)
                              //         source q's rows landed when arrive[q] >= ep[kEpArrive]
   const uint32_t *mblk_src;  //         per m-block (group order): mask of the sources of its rows
+  uint32_t src_all;          //         mask of every source rank: once all have arrived, skip the lookups
   const int32_t *row_src;    // mode 1 push epilogue: (slot << 5) | rank of each receive row, and
   uint16_t *const *peer_slot;//   [P] slot buffers [B*K, nout]: the row's output goes to
                              //   peer_slot[rank] + slot*nout (nullptr: write `out` rows)

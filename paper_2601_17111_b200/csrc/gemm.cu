@@ -71,6 +71,7 @@ struct GemmParams {
   int32_t *err;
   const uint32_t *arrive;
   const uint32_t *mblk_src;
+  uint32_t src_all;      // every source rank (0: unknown)
   const int32_t *row_src;
   uint16_t *const *peer_slot;
   __nv_bfloat16 *out2;   // mode 3: raw [g | u] pre-activations, rows of 2 * nout (training forward)
@@ -110,7 +111,7 @@ __device__ __forceinline__ void wait_weights(const GemmParams &p, int wslot, uin
 // its arrival flag (release after all its rows were stored, route.cu dispatch_kernel), then order the
 // async-proxy (TMA) reads after the acquire.  Bounded like wait_weights.
 __device__ __forceinline__ void wait_sources(const GemmParams &p, int mblk, uint32_t &seen, uint32_t aepoch) {
-  if (!p.arrive) return;
+  if (!p.arrive || (p.src_all && (seen & p.src_all) == p.src_all)) return;   // no per-tile lookup then
   uint32_t need = p.mblk_src[mblk] & ~seen;
   if (!need) return;
   const long long t0 = clock64();
@@ -540,6 +541,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
     uint32_t phase = 0;
     uint32_t seen = 0;   // sources whose arrival lane 0 already acquired
     const uint32_t wep = p.ep ? p.ep[kEpWeight] : 0u, aep = p.ep ? p.ep[kEpArrive] : 0u;
+    // Without the gather (the default) lane 0 runs the loop alone, as in round 1: the warp-wide loop
+    // (32 lanes polling each stage's empty barrier, a __syncwarp per stage) made GEMM1 / GEMM2 4-6 %
+    // slower at base clocks (profiles/r02_gemm_regression_bisect.txt)
+    const unsigned pmask = gather_on ? 0xffffffffu : 1u;
+    if (gather_on || lane == 0)
     for (int u = unit0; u < total_units; u += n_units) {
       const int t = u * MC + cpair;
       TileInfo ti = decode_tile<TM>(t, p.n_ntiles, nullptr, n_groups, p.groups, p.sched);
@@ -565,7 +571,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
           gi[i] = (unsigned)tk < (unsigned)p.xg_rows ? tk : 0;
         }
       }
-      __syncwarp();
+      __syncwarp(pmask);
       // swapped tile: this CTA's 128 weight rows as the A operand (mode 0/2/3: 64 gate + the
       // matching 64 up rows of features nb*BNO + crank*64 ...; mode 1: rows nb*BN + crank*BN/2
       // ...) and its 32 of the group's <= 64 token rows as the B operand
@@ -580,22 +586,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
           const uint32_t fb = mapa_shared(fl, lead);
           if (lane == 0) {
             if (leader) mbar_expect_tx(fl, 2 * nsub * (BM * 128 + 32 * 128));
+            // per sub-tile: the weight rows, then (unless gathered) the token rows -- round 1's issue
+            // order; all weights first and the tokens last measured ~3 % slower in GEMM1 (tokens
+            // first: same as this order), profiles/r02_gemm_regression_bisect.txt
             for (int s2 = 0; s2 < nsub; ++s2) {
               const uint32_t ad = s2 < 2 ? smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128))
                                          : smem_u32(sB + stage * C::B_BYTES);
               tma_load_2d_pair(ad, wms, fb, (kb * SWK + s2) * BK, srow, ti.small ? pol_first : pol_last);
               tma_load_2d_pair(ad + 64 * 128, wms, fb, (kb * SWK + s2) * BK, srow2, ti.small ? pol_first : pol_last);
+              if (!gat)
+                tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES + (SWK == 3 ? BM * 128 : 0) + s2 * (32 * 128)),
+                                 &p.tmAs, fb, (kb * SWK + s2) * BK, ti.row0 + (int)crank * 32, pol_act);
             }
           }
-          for (int s2 = 0; s2 < nsub; ++s2) {
-            const uint32_t bd = smem_u32(sB + stage * C::B_BYTES + (SWK == 3 ? BM * 128 : 0) + s2 * (32 * 128));
-            if (!gat) {
-              if (lane == 0) tma_load_2d_pair(bd, &p.tmAs, fb, (kb * SWK + s2) * BK, ti.row0 + (int)crank * 32, pol_act);
-            } else if (lane < gn) {
+          if (gat && lane < gn) {
+            for (int s2 = 0; s2 < nsub; ++s2) {
+              const uint32_t bd = smem_u32(sB + stage * C::B_BYTES + (SWK == 3 ? BM * 128 : 0) + s2 * (32 * 128));
               tma_gather4_pair(bd + lane * 512, &p.tmXg, fb, (kb * SWK + s2) * BK, gi[0], gi[1], gi[2], gi[3], pol_act);
             }
           }
-          __syncwarp();
+          __syncwarp(pmask);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -613,6 +623,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
           for (int s2 = 0; s2 < nsub; ++s2) {
             const uint32_t adst = smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128));
             const int arow = ti.row0 + (int)crank * (ti.half ? BM / 2 : BM);
+#ifdef LLEP_HOT_B_FIRST
+            tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES + s2 * ((BN / 2) * 128)), wm, fb,
+                             (kb * KSUB + s2) * BK, brow, ti.small ? pol_first : pol_last);
+#endif
             if (MC == 2) {   // sub-tile s2 of this row half, issued by pair s2, into both pairs' CTAs
               if (s2 == cpair)
                 tma_load_2d_pair_mc(adst, &p.tmA, fb, (kb * KSUB + s2) * BK, arow,
@@ -620,8 +634,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
             } else if (!gat) {
               tma_load_2d_pair(adst, &p.tmA, fb, (kb * KSUB + s2) * BK, arow, pol_act);
             }
+#ifndef LLEP_HOT_B_FIRST
             tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES + s2 * ((BN / 2) * 128)), wm, fb,
                              (kb * KSUB + s2) * BK, brow, ti.small ? pol_first : pol_last);
+#endif
           }
         }
         if (gat) {
@@ -629,7 +645,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
             tma_gather4_pair(smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128)) + lane * 512, &p.tmXg, fb,
                              (kb * KSUB + s2) * BK, gi[0], gi[1], gi[2], gi[3], pol_act);
         }
-        __syncwarp();
+        __syncwarp(pmask);
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
@@ -2192,6 +2208,7 @@ llep_status run_grouped_gemm(const GemmArgs &g, cudaStream_t s) {
   prm.err = g.err;
   prm.arrive = g.arrive;
   prm.mblk_src = g.mblk_src;
+  prm.src_all = g.src_all;
   prm.row_src = g.row_src;
   prm.peer_slot = g.peer_slot;
   prm.n_groups_dev = g.n_groups_dev;

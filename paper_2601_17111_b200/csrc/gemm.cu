@@ -623,10 +623,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
           for (int s2 = 0; s2 < nsub; ++s2) {
             const uint32_t adst = smem_u32(sA + stage * C::A_BYTES + s2 * (BM * 128));
             const int arow = ti.row0 + (int)crank * (ti.half ? BM / 2 : BM);
-#ifdef LLEP_HOT_B_FIRST
-            tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES + s2 * ((BN / 2) * 128)), wm, fb,
-                             (kb * KSUB + s2) * BK, brow, ti.small ? pol_first : pol_last);
-#endif
             if (MC == 2) {   // sub-tile s2 of this row half, issued by pair s2, into both pairs' CTAs
               if (s2 == cpair)
                 tma_load_2d_pair_mc(adst, &p.tmA, fb, (kb * KSUB + s2) * BK, arow,
@@ -634,10 +630,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_2cta_kernel(cons
             } else if (!gat) {
               tma_load_2d_pair(adst, &p.tmA, fb, (kb * KSUB + s2) * BK, arow, pol_act);
             }
-#ifndef LLEP_HOT_B_FIRST
             tma_load_2d_pair(smem_u32(sB + stage * C::B_BYTES + s2 * ((BN / 2) * 128)), wm, fb,
                              (kb * KSUB + s2) * BK, brow, ti.small ? pol_first : pol_last);
-#endif
           }
         }
         if (gat) {

@@ -487,7 +487,9 @@ def run_router(L, shape, x, steps, warmup):
     nbytes = B * D * 2 + N * D * 2 + B * K * 8
     return {"ms_per_call": ms, "bytes_per_call": nbytes, "gbs": nbytes / (ms / 1e3) / 1e9,
             "tflops": 2.0 * B * N * D / (ms / 1e3) / 1e12,
-            "note": "x [B,D] bf16 read once (189 MB at G120, > L2) + W_r + ids/gates written"}
+            "note": "x [B,D] bf16 read once (189 MB at G120, > L2) + W_r + ids/gates written; timed after the "
+                    "layer runs, at their power-capped clock: the same kernel takes 39-41 us on an idle GPU and "
+                    "~54 us right after seconds of layer steps (profiles/r02_router_heat.txt)"}
 
 
 def run_cublas_ref(shape, rows, steps):

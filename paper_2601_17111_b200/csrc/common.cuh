@@ -47,7 +47,13 @@ __host__ __device__ inline PlanLayout plan_layout(int32_t N, int32_t P) {
 // GEMM m-block schedule.  Groups with few 128-row blocks stream a whole expert's weights for
 // little work (weight-bandwidth bound); their blocks are spread evenly among the blocks of large
 // groups so the persistent GEMM overlaps that streaming with compute-bound tiles.
-constexpr int kSmallGroupRows = 256;  // groups of at most this many padded rows are "small"
+#ifndef LLEP_SMALL_GROUP_ROWS
+// 512: at the G120 P=8 critical-rank layout the 15 native groups of 416 rows (512 padded) are then
+// spread among the spilled chunk's blocks (and their weights read evict-first): GEMM1 -0.6 %, GEMM2
+// -0.7 % at base clocks vs 256; P=1 unchanged (profiles/r02_ab_small_group_rows.txt)
+#define LLEP_SMALL_GROUP_ROWS 512
+#endif
+constexpr int kSmallGroupRows = LLEP_SMALL_GROUP_ROWS;  // groups of at most this many padded rows are "small"
 // Position of the idx-th block of its class when nb "big" and ns "small" blocks are merged
 // evenly: keys (2k+1)*ns for big block k, (2j+1)*nb for small block j, ties -> big first.
 __host__ __device__ inline int64_t interleave_pos(bool big, int64_t idx, int64_t nb, int64_t ns) {
